@@ -1,0 +1,84 @@
+"""O2 / O2' -- block statistics (oracle; test infrastructure only).
+
+O2' EXACT (§4.1 Eq. 2): S_(i,j) = (1/B^2) sum_{x,y} 1(A_(iB+x, jB+y) < eta),
+   with A the post-softmax attention map (reading Z2, Alg. 1 P:995 "A = softmax(QK^T/sqrt d)"),
+   strict "<", eta = 1e-4 (App. A).  Ragged blocks divide by |I_i||I_j| (Z16).
+   Informativeness polarity (reading Z3): U = 1 - S ("less S = more informative").
+
+O2 POOLED (BASELINE.json north_star (1); the hot-path substitute for Eq. 2, reading Z1):
+   qbar_i = mean_{p in I_i} Q_p, kbar_j likewise; z_ij = s * qbar_i . kbar_j, s = 1/sqrt(D)
+   (P:106); W_ij = |I_j| e^{z_ij} / sum_j' |I_j'| e^{z_ij'}  (block mass of the pooled
+   surrogate: every key of block j scores z_ij).  U = W.
+   -- parity unpinned against the paper (north-star construct); pinned by identities in
+   tests/test_oracle_stats.py.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .layout import Layout
+
+
+def _f64(x):
+    import torch
+    if isinstance(x, torch.Tensor):
+        return x.detach().to("cpu", dtype=torch.float64).numpy()
+    return np.asarray(x, dtype=np.float64)
+
+
+def pooled_block_stats(q, k, L: Layout, scale: float | None = None, return_z: bool = False):
+    """POOLED statistic W [B,H,n,n] (fp64) from Q, K [B,H,N,D]."""
+    q = _f64(q)
+    k = _f64(k)
+    s = 1.0 / np.sqrt(L.head_dim) if not scale else float(scale)
+    n = L.n
+    sizes = np.array([L.block_size(i) for i in range(n)], dtype=np.float64)
+    B, H = q.shape[0], q.shape[1]
+    qbar = np.empty((B, H, n, L.head_dim))
+    kbar = np.empty((B, H, n, L.head_dim))
+    for i in range(n):
+        lo, hi = L.block_range(i)
+        qbar[:, :, i] = q[:, :, lo:hi].mean(axis=2)
+        kbar[:, :, i] = k[:, :, lo:hi].mean(axis=2)
+    z = s * np.einsum("bhid,bhjd->bhij", qbar, kbar)
+    logits = z + np.log(sizes)[None, None, None, :]
+    m = logits.max(axis=-1, keepdims=True)
+    e = np.exp(logits - m)
+    W = e / e.sum(axis=-1, keepdims=True)
+    return (W, z) if return_z else W
+
+
+def exact_sparsity(q, k, L: Layout, eta: float = 1e-4, scale: float | None = None):
+    """EXACT Eq. 2 sparsity map S [B,H,n,n] from the full post-softmax map (tiny shapes only)."""
+    q = _f64(q)
+    k = _f64(k)
+    s = 1.0 / np.sqrt(L.head_dim) if not scale else float(scale)
+    B, H, N, _ = q.shape
+    n = L.n
+    S = np.zeros((B, H, n, n))
+    for b in range(B):
+        for h in range(H):
+            A = s * q[b, h] @ k[b, h].T
+            A = np.exp(A - A.max(axis=1, keepdims=True))
+            A /= A.sum(axis=1, keepdims=True)                      # P:995 post-softmax map
+            S[b, h] = sparsity_from_map(A, L, eta)
+    return S
+
+
+def sparsity_from_map(A, L: Layout, eta: float = 1e-4):
+    """Eq. 2 on one N x N attention map: fraction of entries strictly below eta per block."""
+    A = np.asarray(A, dtype=np.float64)
+    n = L.n
+    below = (A < eta)
+    S = np.zeros((n, n))
+    for i in range(n):
+        ilo, ihi = L.block_range(i)
+        for j in range(n):
+            jlo, jhi = L.block_range(j)
+            S[i, j] = below[ilo:ihi, jlo:jhi].sum() / ((ihi - ilo) * (jhi - jlo))
+    return S
+
+
+def informativeness_from_sparsity(S):
+    """Reading Z3: U = 1 - S (larger = more informative)."""
+    return 1.0 - np.asarray(S, dtype=np.float64)

@@ -1,0 +1,83 @@
+"""Pins for oracle O2 (pooled statistic) and O2' (Eq. 2 sparsity) -- no GPU.
+
+O2 has no paper anchor (north-star construct, "parity unpinned" vs the paper); it is pinned here
+by identities: z_ij equals the block mean of the token scores s Q_p . K_q (brute force), rows of
+W sum to 1, the closed form for block-constant Q/K, and the uniform case Q = 0.
+O2' is pinned by SPEC.md S:106-111 examples and monotonicity in eta.
+"""
+import math
+
+import numpy as np
+import torch
+
+import oracle as O
+
+
+def _lay():
+    return O.make_layout(1, 2, 8, 3, 3, 2, 5, 4)     # N = 33, ragged last block, prefix
+
+
+def test_pooled_z_is_block_mean_of_token_scores():
+    L = _lay()
+    g = torch.Generator().manual_seed(0)
+    q = torch.randn((1, 2, L.N, 8), generator=g, dtype=torch.float64)
+    k = torch.randn((1, 2, L.N, 8), generator=g, dtype=torch.float64)
+    W, z = O.pooled_block_stats(q, k, L, return_z=True)
+    s = 1 / math.sqrt(8)
+    qn, kn = q.numpy(), k.numpy()
+    for h in range(2):
+        T = s * qn[0, h] @ kn[0, h].T
+        for i in range(L.n):
+            for j in range(L.n):
+                (a, b), (c, d) = L.block_range(i), L.block_range(j)
+                assert abs(T[a:b, c:d].mean() - z[0, h, i, j]) <= 1e-13
+    assert np.allclose(W.sum(-1), 1.0, atol=1e-14)
+
+
+def test_pooled_closed_form_constant_blocks():
+    L = _lay()
+    rng = np.random.default_rng(1)
+    qb, kb = rng.standard_normal((L.n, 8)), rng.standard_normal((L.n, 8))
+    tb = np.arange(L.N) // L.block
+    q = np.broadcast_to(qb[tb], (1, 2, L.N, 8)).copy()
+    k = np.broadcast_to(kb[tb], (1, 2, L.N, 8)).copy()
+    W = O.pooled_block_stats(q, k, L)
+    sizes = np.array([L.block_size(i) for i in range(L.n)])
+    # every token pair (p,q) in block (i,j) scores s qb_i . kb_j: softmax mass of block j
+    for i in range(L.n):
+        e = sizes * np.exp(qb[i] @ kb.T / math.sqrt(8))
+        assert np.allclose(W[0, 0, i], e / e.sum(), atol=1e-14)
+
+
+def test_pooled_uniform_when_q_zero():
+    L = _lay()
+    q = np.zeros((1, 2, L.N, 8))
+    k = np.random.default_rng(2).standard_normal((1, 2, L.N, 8))
+    W = O.pooled_block_stats(q, k, L)
+    sizes = np.array([L.block_size(i) for i in range(L.n)])
+    assert np.allclose(W, sizes / L.N, atol=1e-15)
+
+
+def test_sparsity_spec_examples():
+    L = O.make_layout(1, 1, 8, 0, 1, 1, 256, 128)
+    assert np.array_equal(O.sparsity_from_map(np.zeros((256, 256)), L), np.ones((2, 2)))
+    assert np.array_equal(O.sparsity_from_map(np.ones((256, 256)), L), np.zeros((2, 2)))
+    L4 = O.make_layout(1, 1, 8, 0, 1, 1, 4, 2)
+    A = np.ones((4, 4))
+    A[0, 0] = A[0, 1] = 0.0
+    A[1, 0], A[1, 1] = 0.5, 0.5
+    assert O.sparsity_from_map(A, L4)[0, 0] == 0.5
+
+
+def test_sparsity_monotone_in_eta():
+    L = _lay()
+    rng = np.random.default_rng(3)
+    q = rng.standard_normal((1, 2, L.N, 8)) * 2
+    k = rng.standard_normal((1, 2, L.N, 8)) * 2
+    prev = None
+    for eta in (1e-6, 1e-4, 1e-2, 1e-1):
+        S = O.exact_sparsity(q, k, L, eta)
+        assert np.all((S >= 0) & (S <= 1))
+        if prev is not None:
+            assert np.all(prev <= S)
+        prev = S
