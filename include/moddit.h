@@ -1,0 +1,170 @@
+/*
+ * moddit.h -- C ABI of the B200 (sm_100a) MOD-DiT hot path (arxiv 2601.11641).
+ *
+ * The five compute calls follow the paper's statement of the problem (Algorithm 1, PAPER.md
+ * P:983-1033) and BASELINE.json north_star:
+ *     mod_collect_block_stats   block statistic of Q, K            (north_star (1); Eq. 2 P:204-206 is
+ *                                                                   the paper's statistic, Z1)
+ *     mod_fit_mixture           least-squares mixture fit, Eq. 4   (App. B)
+ *     mod_keep_frames           block-diagonal preservation        (§5.3; Alg. 1)
+ *     mod_predict_block_mask    linear prediction + selection + CSR (Eq. 6/7 P:335-337, P:418-420;
+ *                                                                   §5.3; Alg. 1)
+ *     mod_update_online_mask    Eq. 5 reconstruction + refit + roll (Alg. 1)
+ *     mod_block_sparse_attn_fwd block-sparse attention forward     (Eq. 1; §5.4)
+ *
+ * Conventions
+ *  - Every pointer is a DEVICE pointer unless marked (host).  Tensors are dense, contiguous,
+ *    row-major, 16-byte aligned (Q/K/V/O 128-byte aligned for TMA).
+ *  - Q, K, V, O: bf16 [B, H, N, D].  Token order inside a head: [prefix | frame-major, y, x],
+ *    N = prefix_tokens + frames*height*width.
+ *  - n = ceil(N / block) blocks; block i holds tokens [i*block, min((i+1)*block, N)).
+ *  - p = 3n - 1 + frames intensities per head, ordered C_0..C_{2n-2} (offset delta_k = k-(n-1)),
+ *    D_0..D_{n-1} (column k), E_0..E_{F-1} (frame square r)  (reading Z4).
+ *  - Block statistic / history maps: fp32 [B, H, n, n] row-major; intensities fp64 [B, H, p].
+ *  - Block masks are per-head CSR index lists: row_ptr int32 [B, H, n+1] holding offsets local to
+ *    the head (row_ptr[..,0] = 0, row_ptr[..,n] = nnz of that head), col_idx int32 [B, H, n*n]
+ *    (capacity n*n per head; entries [row_ptr[i], row_ptr[i+1]) are the ascending passing columns).
+ *  - Every compute call is asynchronous and stream-ordered on `stream` (a cudaStream_t; 0 =
+ *    legacy default stream).  Only mod_plan_create synchronizes.
+ *  - Ownership: the caller allocates every tensor and the workspace `ws` (size from
+ *    mod_plan_workspace_bytes); the library allocates device memory only inside
+ *    mod_plan_create (constant tables) and frees it in mod_plan_destroy.  Nothing is retained
+ *    after a call returns.  A plan is immutable after creation and may be used concurrently from
+ *    several host threads / streams provided each concurrent call has its own workspace.
+ *  - Errors: host-side validation runs before any launch.  A failing call launches nothing,
+ *    returns the status and sets a thread-local message (mod_last_error) naming the argument
+ *    and the values.  Asynchronous device faults surface as MOD_ERR_CUDA on a later call.
+ *    There is no CPU fallback: on a device other than sm_100 the plan fails with
+ *    MOD_ERR_UNSUPPORTED.
+ *  - Determinism: no floating-point atomics; two runs on the same inputs are bitwise identical.
+ */
+#ifndef MODDIT_H_
+#define MODDIT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MOD_OK = 0,
+  MOD_ERR_USAGE = 1,       /* null required pointer, bad enum, bad handle */
+  MOD_ERR_INPUT = 2,       /* shape / layout / range violation */
+  MOD_ERR_NUMERICAL = 3,   /* plan factorization failed (App. B P:1251-1270 chain exhausted) */
+  MOD_ERR_CUDA = 4,        /* CUDA runtime / driver error (incl. earlier async faults) */
+  MOD_ERR_UNSUPPORTED = 5  /* device is not sm_100 / missing driver entry point */
+} mod_status;
+
+/* Selection rule over the 3n-1 pool of predicted C/D intensities (§5.3, reading Z3/Z14):
+ * keys are sorted descending ("informativeness" polarity), ties by ascending pattern id. */
+typedef enum {
+  MOD_SELECT_TOPK = 0,      /* the K largest keys (the paper's Top-K router) */
+  MOD_SELECT_THRESHOLD = 1, /* keys > select_param (north_star "threshold selection") */
+  MOD_SELECT_TOPMASS = 2    /* shortest sorted prefix whose sum of max(key,0)*|supp| reaches
+                               select_param * total (north_star "top-mass selection") */
+} mod_select_mode;
+
+typedef enum {
+  MOD_STAT_POOLED = 0       /* north_star (1): mean-pooled q.k block score + row softmax mass */
+} mod_stat_mode;
+
+typedef struct {
+  int32_t batch, heads, head_dim;  /* B, H, D; D in {64, 128} */
+  int32_t prefix_tokens;           /* P0 >= 0 (226 for CogVideoX text tokens) */
+  int32_t frames, height, width;   /* latent F, Hh, Ww; N = P0 + F*Hh*Ww */
+  int32_t block;                   /* 128, or 64 */
+} mod_layout;
+
+typedef struct {
+  double lambda;        /* Tikhonov parameter, 1e-8 (App. B) */
+  float tau_e;          /* block-diagonal threshold; reading Z7 default 0 */
+  int32_t top_k;        /* default K for MOD_SELECT_TOPK (App. C) */
+  int32_t select_mode;  /* mod_select_mode default */
+  float select_param;   /* default threshold / mass fraction */
+  int32_t stat_mode;    /* mod_stat_mode */
+  int32_t masked_renorm;/* 1: Eq. 5 uses the fresh map renormalised over the selected blocks (Z12) */
+  int32_t diag_guard;   /* 1: every row keeps block (i,i) (reading Z15) */
+  float softmax_scale;  /* 0 -> 1/sqrt(D) */
+} mod_config;
+
+/* Per-call selection override for mod_predict_block_mask (nullable: plan defaults). */
+typedef struct {
+  int32_t select_mode;
+  int32_t top_k;
+  float select_param;
+} mod_selection;
+
+typedef struct mod_plan_s* mod_plan;
+
+/* Builds the per-layout constants on `device` and synchronizes:
+ *   frame block ranges [a_r,b_r] = [floor((P0+r*HW)/block), floor((P0+(r+1)*HW-1)/block)] (Z5);
+ *   the closed-form Gram G = M^T M + lambda*I (App. B, plus counted C^T E, D^T E,
+ *   overlapping E^T E) and its inverse after deflating the analytically known null space of M
+ *   (DESIGN.md "Fit numerics"): fp64 p x p, p^2*8 bytes of device memory.
+ * Returns MOD_ERR_INPUT for a bad layout, MOD_ERR_NUMERICAL if the deflated Gram is not
+ * numerically positive definite, MOD_ERR_UNSUPPORTED if `device` is not sm_100. */
+mod_status mod_plan_create(const mod_layout* layout /*host*/, const mod_config* cfg /*host*/, int device,
+                           mod_plan* out /*host*/);
+void mod_plan_destroy(mod_plan plan);
+size_t mod_plan_workspace_bytes(mod_plan plan);
+int32_t mod_plan_num_blocks(mod_plan plan);   /* n */
+int32_t mod_plan_num_patterns(mod_plan plan); /* p = 3n - 1 + F */
+/* Copies the frame block ranges: a_b (host) receives 2*F ints (a_0,b_0,a_1,b_1,...). */
+mod_status mod_plan_frame_blocks(mod_plan plan, int32_t* a_b /*host*/);
+/* Smallest pivot met while inverting the deflated Gram (host out) and the dimension of the deflated
+ * analytic null space (host out).  A min pivot of order lambda flags a dependency the analytic list
+ * missed (degenerate tiny layouts); X then carries the undeflated ~cond(G)*eps error. */
+mod_status mod_plan_diagnostics(mod_plan plan, double* min_pivot, int32_t* null_dim);
+/* Device pointer to the fp64 deflated Gram inverse (p x p), for diagnostics. */
+const double* mod_plan_gram_inverse(mod_plan plan);
+const char* mod_last_error(void);
+const char* mod_version(void);
+
+/* K1: W[b,h,i,j] = |I_j| exp(z_ij) / sum_j' |I_j'| exp(z_ij'),  z_ij = s * qbar_i . kbar_j,
+ * qbar_i = mean_{p in I_i} Q_p (fp32 accumulation), s = softmax_scale.
+ * q, k: bf16 [B,H,N,D]; stats: out fp32 [B,H,n,n]. */
+mod_status mod_collect_block_stats(mod_plan plan, const void* q, const void* k, float* stats, void* ws,
+                                   void* stream);
+
+/* K2a: X = G^-1 M^T vec(U) per head, U = stats (fp32 [B,H,n,n]); x: out fp64 [B,H,p];
+ * nae: nullable out fp32 [B,H] = ||U - MX||_F / ||U||_F (§4.2). */
+mod_status mod_fit_mixture(mod_plan plan, const float* stats, double* x, float* nae, void* ws, void* stream);
+
+/* keep[b,h,r] = min(e_r(x_a), e_r(x_b)) > tau_e  (uint8 [B,H,F]). */
+mod_status mod_keep_frames(mod_plan plan, const double* x_a, const double* x_b, uint8_t* keep, void* stream);
+
+/* K2b: x_hat = x_curr + (x_curr - x_prev)/(t_curr - t_prev)*(t - t_curr) on the C,D parts (IEEE fp64,
+ * no FMA contraction), selection over the 3n-1 pool, block mask = union of selected supports,
+ * kept frame squares, the diagonal guard and the prefix rows/columns, emitted as CSR.
+ * Requires t_prev != t_curr.  keep may be NULL (no frame squares). */
+mod_status mod_predict_block_mask(mod_plan plan, const double* x_prev, const double* x_curr, int32_t t_prev,
+                                  int32_t t_curr, int32_t t, const uint8_t* keep, const mod_selection* sel /*host,
+                                  nullable*/, int32_t* row_ptr, int32_t* col_idx, void* ws, void* stream);
+
+/* K3: for every selected (i,j) of the CSR mask: hist[i,j] = stats[i,j] / sum_{j' selected} stats[i,j']
+ * (masked_renorm=1) or stats[i,j] (0); unselected entries keep their history bit-for-bit (Eq. 5).
+ * Then X = fit(hist); x_prev <- x_curr; x_curr <- X. */
+mod_status mod_update_online_mask(mod_plan plan, const float* stats_fresh, const int32_t* row_ptr,
+                                  const int32_t* col_idx, float* stats_hist, double* x_prev, double* x_curr,
+                                  void* ws, void* stream);
+
+/* K4: for token p of query block i: O_p = sum_{q in K(i)} softmax(s Q_p.K_q) V_q over the keys of
+ * the listed blocks (keys >= N masked), lse_p = ln sum exp(s Q_p.K_q); an empty list gives O = 0,
+ * lse = -inf (Z15).  bf16 inputs, fp32 accumulation and softmax (tcgen05 + TMEM), bf16 output.
+ * o: out bf16 [B,H,N,D]; lse: nullable out fp32 [B,H,N].  Column indices must be < n. */
+mod_status mod_block_sparse_attn_fwd(mod_plan plan, const void* q, const void* k, const void* v,
+                                     const int32_t* row_ptr, const int32_t* col_idx, void* o, float* lse,
+                                     void* ws, void* stream);
+
+/* Dense mask helper (the warm-up's full attention, Alg. 1): all-ones CSR. */
+mod_status mod_fill_dense_mask(mod_plan plan, int32_t* row_ptr, int32_t* col_idx, void* stream);
+
+/* Number of kernels the last successful compute call on this thread launched (for bench.py). */
+int32_t mod_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MODDIT_H_ */

@@ -1,0 +1,96 @@
+// common.cuh -- shared plumbing of libmoddit (plan struct, error handling, sm_100a PTX wrappers).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string>
+#include <vector>
+
+#include "../../include/moddit.h"
+
+// ------------------------------------------------------------------------------------------------
+// error handling (thread-local message, see mod_last_error)
+// ------------------------------------------------------------------------------------------------
+void mod_set_error(const char* fmt, ...);
+void mod_note_launches(int n);
+
+#define MOD_REQUIRE(cond, status, ...)     \
+  do {                                     \
+    if (!(cond)) {                         \
+      mod_set_error(__VA_ARGS__);          \
+      return (status);                     \
+    }                                      \
+  } while (0)
+
+#define MOD_CUDA(call)                                                                    \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess) {                                                              \
+      mod_set_error("CUDA error %s at %s:%d: %s", cudaGetErrorName(e_), __FILE__, __LINE__, \
+                    cudaGetErrorString(e_));                                              \
+      return MOD_ERR_CUDA;                                                                \
+    }                                                                                     \
+  } while (0)
+
+// Checks for an earlier asynchronous fault before launching, and for a launch error after.
+mod_status mod_check_sticky();
+#define MOD_LAUNCH_CHECK() MOD_CUDA(cudaGetLastError())
+
+// ------------------------------------------------------------------------------------------------
+// plan
+// ------------------------------------------------------------------------------------------------
+struct mod_plan_s {
+  mod_layout L;
+  mod_config cfg;
+  int device;
+  int N, n, p, F, prefix_last;  // prefix_last = last prefix block or -1
+  float scale;                  // softmax scale s
+  std::vector<int> frame_ab;    // host [2F]
+  int* d_frame_ab;              // device [2F]
+  int* d_row_frames;            // device [2n]: frames containing block i are [lo, hi] (hi < lo: none)
+  float* d_log_sizes;           // device [n]: ln |I_j|
+  double* d_ginv;               // device [p*p] deflated Gram inverse
+  size_t ws_bytes;
+  // workspace carve (byte offsets)
+  size_t ws_qbar, ws_kbar, ws_part, ws_r, ws_x, ws_nae;
+  int proj_tiles;               // row tiles of the projection kernel
+  int sm_count;
+  double min_pivot;             // smallest Gauss-Jordan pivot of the deflated Gram
+  int null_dim;                 // dimension of the deflated (analytic) null space
+};
+
+mod_status mod_validate_plan(mod_plan plan);
+
+static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+constexpr int kProjRows = 32;    // rows per projection tile (fit / update)
+constexpr int kMaxBlocks = 2048; // n limit (pattern pool 3n-1 sorted in shared memory)
+
+// ------------------------------------------------------------------------------------------------
+// device helpers
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ float warp_sum_f(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max_f(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ int4 ld_nc_v4(const void* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}

@@ -1,0 +1,353 @@
+// plan.cu -- mod_plan_create / destroy, error plumbing, and the per-layout constants.
+//
+// The plan holds everything that depends only on the layout (App. B: the Gram matrix
+// M^T M "can be computed analytically ... without explicit matrix construction", and
+// is shared by every head and step):
+//   * frame block ranges [a_r, b_r] (reading Z5) and, per block, the frames containing it;
+//   * ln|I_j| for the pooled block-mass softmax (north_star (1));
+//   * the inverse of the Tikhonov Gram G = M^T M + lambda I (App. B), computed after
+//     deflating the analytically known null space N of M: G' = G + c V V^T with V an orthonormal
+//     basis of N.  Because r = M^T vec U is orthogonal to N, G'^{-1} r = G^{-1} r exactly, while
+//     cond(G') ~ 1e2 instead of cond(G) ~ 1e10.  The inverse is formed
+//     once on the device by fp64 Gauss-Jordan elimination (G' is SPD, no pivoting needed).
+#include <cmath>
+#include <cstdarg>
+#include <cstring>
+#include <map>
+
+#include "common.cuh"
+
+static thread_local char g_err[1024] = "";
+static thread_local int g_launches = 0;
+
+void mod_set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+void mod_note_launches(int n) { g_launches = n; }
+
+extern "C" const char* mod_last_error(void) { return g_err; }
+extern "C" const char* mod_version(void) { return "moddit-b200 0.1 (sm_100a)"; }
+extern "C" int32_t mod_last_launch_count(void) { return g_launches; }
+
+mod_status mod_check_sticky() {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    mod_set_error("pending CUDA error before launch: %s (%s)", cudaGetErrorName(e), cudaGetErrorString(e));
+    return MOD_ERR_CUDA;
+  }
+  return MOD_OK;
+}
+
+mod_status mod_validate_plan(mod_plan plan) {
+  MOD_REQUIRE(plan != nullptr, MOD_ERR_USAGE, "plan is NULL");
+  MOD_REQUIRE(plan->d_ginv != nullptr, MOD_ERR_USAGE, "plan is not initialised");
+  return mod_check_sticky();
+}
+
+// ------------------------------------------------------------------------------------------------
+// Gauss-Jordan inversion (fp64, in place, no pivoting: the deflated Gram is SPD)
+// ------------------------------------------------------------------------------------------------
+__global__ void gj_pivot_kernel(double* A, double* col, double* pivots, int p, int k) {
+  __shared__ double piv;
+  if (threadIdx.x == 0) {
+    piv = A[(size_t)k * p + k];
+    pivots[k] = piv;
+  }
+  __syncthreads();
+  const double inv = 1.0 / piv;
+  for (int i = threadIdx.x; i < p; i += blockDim.x) col[i] = (i == k) ? 0.0 : A[(size_t)i * p + k];
+  __syncthreads();
+  for (int j = threadIdx.x; j < p; j += blockDim.x) {
+    double a = (j == k) ? 1.0 : A[(size_t)k * p + j];
+    A[(size_t)k * p + j] = a * inv;
+  }
+}
+
+__global__ void gj_eliminate_kernel(double* A, const double* col, int p, int k) {
+  const int i = blockIdx.y;
+  if (i == k) return;
+  const double f = col[i];
+  const double* rk = A + (size_t)k * p;
+  double* ri = A + (size_t)i * p;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < p; j += gridDim.x * blockDim.x) {
+    double a = (j == k) ? 0.0 : ri[j];
+    ri[j] = a - f * rk[j];
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// host: closed-form Gram (App. B; C^T E, D^T E and overlapping E^T E by counting)
+// ------------------------------------------------------------------------------------------------
+static void build_gram(int n, const std::vector<int>& ab, double lambda, std::vector<double>& G) {
+  const int F = (int)ab.size() / 2;
+  const int p = 3 * n - 1 + F;
+  const int oC = 0, oD = 2 * n - 1, oE = 3 * n - 1;
+  G.assign((size_t)p * p, 0.0);
+  auto at = [&](int i, int j) -> double& { return G[(size_t)i * p + j]; };
+  for (int k = 0; k < 2 * n - 1; ++k) {
+    const int d = k - (n - 1);
+    at(oC + k, oC + k) = n - std::abs(d);
+    for (int j = 0; j < n; ++j)
+      if (j - d >= 0 && j - d <= n - 1) at(oC + k, oD + j) = at(oD + j, oC + k) = 1.0;
+    for (int r = 0; r < F; ++r) {
+      const int Lr = ab[2 * r + 1] - ab[2 * r] + 1;
+      const double v = std::max(0, Lr - std::abs(d));
+      at(oC + k, oE + r) = at(oE + r, oC + k) = v;
+    }
+  }
+  for (int j = 0; j < n; ++j) {
+    at(oD + j, oD + j) = n;
+    for (int r = 0; r < F; ++r)
+      if (ab[2 * r] <= j && j <= ab[2 * r + 1]) at(oD + j, oE + r) = at(oE + r, oD + j) = ab[2 * r + 1] - ab[2 * r] + 1;
+  }
+  for (int r = 0; r < F; ++r)
+    for (int s = 0; s < F; ++s) {
+      const int ov = std::max(0, std::min(ab[2 * r + 1], ab[2 * s + 1]) - std::max(ab[2 * r], ab[2 * s]) + 1);
+      at(oE + r, oE + s) = (double)ov * ov;
+    }
+  for (int i = 0; i < p; ++i) at(i, i) += lambda;
+}
+
+// Analytic null space of M (linear dependencies among the binary bases), see DESIGN.md:
+//   sum_k C_k = J = sum_k D_k;  a square covering the whole grid equals J;  unit squares covering
+//   every diagonal block sum to C_{delta=0};  identical squares are equal columns.
+static std::vector<std::vector<double>> null_space(int n, const std::vector<int>& ab) {
+  const int F = (int)ab.size() / 2;
+  const int p = 3 * n - 1 + F;
+  const int oC = 0, oD = 2 * n - 1, oE = 3 * n - 1;
+  std::vector<std::vector<double>> V;
+  {
+    std::vector<double> v(p, 0.0);
+    for (int k = 0; k < 2 * n - 1; ++k) v[oC + k] = 1.0;
+    for (int k = 0; k < n; ++k) v[oD + k] = -1.0;
+    V.push_back(v);
+  }
+  std::map<std::pair<int, int>, int> first;
+  for (int r = 0; r < F; ++r) {
+    auto key = std::make_pair(ab[2 * r], ab[2 * r + 1]);
+    auto it = first.find(key);
+    if (it == first.end()) {
+      first[key] = r;
+    } else {
+      std::vector<double> v(p, 0.0);
+      v[oE + r] = 1.0;
+      v[oE + it->second] = -1.0;
+      V.push_back(v);
+    }
+  }
+  for (auto& kv : first) {
+    if (kv.first.first == 0 && kv.first.second == n - 1) {
+      std::vector<double> v(p, 0.0);
+      for (int k = 0; k < 2 * n - 1; ++k) v[oC + k] = 1.0;
+      v[oE + kv.second] = -1.0;
+      V.push_back(v);
+    }
+  }
+  {
+    bool all_unit = true;
+    std::vector<int> rep(n, -1);
+    for (auto& kv : first) {
+      if (kv.first.first != kv.first.second) all_unit = false;
+      else rep[kv.first.first] = kv.second;
+    }
+    bool covers = all_unit;
+    for (int i = 0; i < n && covers; ++i) covers = rep[i] >= 0;
+    if (covers && n > 1) {
+      std::vector<double> v(p, 0.0);
+      v[oC + (n - 1)] = 1.0;
+      for (int i = 0; i < n; ++i) v[oE + rep[i]] = -1.0;
+      V.push_back(v);
+    }
+  }
+  // orthonormalise (modified Gram-Schmidt, twice)
+  std::vector<std::vector<double>> Q;
+  for (auto v : V) {
+    for (int pass = 0; pass < 2; ++pass)
+      for (auto& q : Q) {
+        double d = 0;
+        for (int i = 0; i < p; ++i) d += q[i] * v[i];
+        for (int i = 0; i < p; ++i) v[i] -= d * q[i];
+      }
+    double nr = 0;
+    for (int i = 0; i < p; ++i) nr += v[i] * v[i];
+    nr = std::sqrt(nr);
+    if (nr < 1e-9) continue;
+    for (int i = 0; i < p; ++i) v[i] /= nr;
+    Q.push_back(v);
+  }
+  return Q;
+}
+
+static size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+extern "C" mod_status mod_plan_create(const mod_layout* layout, const mod_config* cfg, int device, mod_plan* out) {
+  MOD_REQUIRE(layout && cfg && out, MOD_ERR_USAGE, "mod_plan_create: layout, cfg and out must be non-NULL");
+  *out = nullptr;
+  const mod_layout L = *layout;
+  MOD_REQUIRE(L.batch >= 1 && L.heads >= 1, MOD_ERR_INPUT, "batch=%d heads=%d must be >= 1", L.batch, L.heads);
+  MOD_REQUIRE(L.head_dim == 64 || L.head_dim == 128, MOD_ERR_INPUT, "head_dim=%d must be 64 or 128", L.head_dim);
+  MOD_REQUIRE(L.block == 64 || L.block == 128, MOD_ERR_INPUT, "block=%d must be 64 or 128", L.block);
+  MOD_REQUIRE(L.prefix_tokens >= 0 && L.frames >= 1 && L.height >= 1 && L.width >= 1, MOD_ERR_INPUT,
+              "prefix_tokens=%d frames=%d height=%d width=%d invalid", L.prefix_tokens, L.frames, L.height, L.width);
+  const long long Nll = (long long)L.prefix_tokens + (long long)L.frames * L.height * L.width;
+  MOD_REQUIRE(Nll <= (1 << 26), MOD_ERR_INPUT, "N=%lld too large", Nll);
+  const int N = (int)Nll;
+  const int n = (N + L.block - 1) / L.block;
+  MOD_REQUIRE(n <= kMaxBlocks, MOD_ERR_INPUT, "n=%d blocks exceeds the supported %d", n, kMaxBlocks);
+  MOD_REQUIRE(cfg->lambda >= 0.0 && std::isfinite(cfg->lambda), MOD_ERR_INPUT, "lambda=%g must be >= 0", cfg->lambda);
+  MOD_REQUIRE(cfg->top_k >= 1, MOD_ERR_INPUT, "top_k=%d must be >= 1", cfg->top_k);
+  MOD_REQUIRE(cfg->select_mode >= 0 && cfg->select_mode <= 2, MOD_ERR_USAGE, "select_mode=%d invalid", cfg->select_mode);
+  MOD_REQUIRE(cfg->stat_mode == MOD_STAT_POOLED, MOD_ERR_UNSUPPORTED, "stat_mode=%d not supported", cfg->stat_mode);
+  MOD_REQUIRE(cfg->softmax_scale >= 0.f, MOD_ERR_INPUT, "softmax_scale=%g must be >= 0", cfg->softmax_scale);
+
+  int ndev = 0;
+  MOD_CUDA(cudaGetDeviceCount(&ndev));
+  MOD_REQUIRE(device >= 0 && device < ndev, MOD_ERR_USAGE, "device=%d out of range (%d devices)", device, ndev);
+  cudaDeviceProp prop;
+  MOD_CUDA(cudaGetDeviceProperties(&prop, device));
+  MOD_REQUIRE(prop.major == 10 && prop.minor == 0, MOD_ERR_UNSUPPORTED,
+              "device %d is sm_%d%d; this library is built for sm_100a (B200) only", device, prop.major, prop.minor);
+  int prev_dev = 0;
+  MOD_CUDA(cudaGetDevice(&prev_dev));
+  MOD_CUDA(cudaSetDevice(device));
+
+  mod_plan P = new mod_plan_s{};
+  P->L = L;
+  P->cfg = *cfg;
+  P->device = device;
+  P->N = N;
+  P->n = n;
+  P->F = L.frames;
+  P->p = 3 * n - 1 + L.frames;
+  P->prefix_last = L.prefix_tokens > 0 ? (L.prefix_tokens - 1) / L.block : -1;
+  P->scale = cfg->softmax_scale > 0.f ? cfg->softmax_scale : 1.0f / std::sqrt((float)L.head_dim);
+  P->sm_count = prop.multiProcessorCount;
+  const int HW = L.height * L.width;
+  P->frame_ab.resize(2 * L.frames);
+  for (int r = 0; r < L.frames; ++r) {
+    P->frame_ab[2 * r] = (L.prefix_tokens + r * HW) / L.block;
+    P->frame_ab[2 * r + 1] = (L.prefix_tokens + (r + 1) * HW - 1) / L.block;
+  }
+  std::vector<int> row_frames(2 * n);
+  for (int i = 0; i < n; ++i) {
+    int lo = L.frames, hi = -1;
+    for (int r = 0; r < L.frames; ++r)
+      if (P->frame_ab[2 * r] <= i && i <= P->frame_ab[2 * r + 1]) {
+        lo = std::min(lo, r);
+        hi = std::max(hi, r);
+      }
+    row_frames[2 * i] = lo;
+    row_frames[2 * i + 1] = hi;
+  }
+  std::vector<float> logsz(n);
+  for (int j = 0; j < n; ++j) logsz[j] = std::log((float)(std::min((j + 1) * L.block, N) - j * L.block));
+
+  auto fail = [&](mod_status st) {
+    mod_plan_destroy(P);
+    cudaSetDevice(prev_dev);
+    return st;
+  };
+#define PLAN_CUDA(call)                                                                            \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess) {                                                                       \
+      mod_set_error("CUDA error %s in mod_plan_create: %s", cudaGetErrorName(e_), cudaGetErrorString(e_)); \
+      return fail(MOD_ERR_CUDA);                                                                   \
+    }                                                                                              \
+  } while (0)
+
+  PLAN_CUDA(cudaMalloc(&P->d_frame_ab, sizeof(int) * 2 * L.frames));
+  PLAN_CUDA(cudaMemcpy(P->d_frame_ab, P->frame_ab.data(), sizeof(int) * 2 * L.frames, cudaMemcpyHostToDevice));
+  PLAN_CUDA(cudaMalloc(&P->d_row_frames, sizeof(int) * 2 * n));
+  PLAN_CUDA(cudaMemcpy(P->d_row_frames, row_frames.data(), sizeof(int) * 2 * n, cudaMemcpyHostToDevice));
+  PLAN_CUDA(cudaMalloc(&P->d_log_sizes, sizeof(float) * n));
+  PLAN_CUDA(cudaMemcpy(P->d_log_sizes, logsz.data(), sizeof(float) * n, cudaMemcpyHostToDevice));
+
+  // ---- deflated Gram and its inverse
+  const int p = P->p;
+  std::vector<double> G;
+  build_gram(n, P->frame_ab, cfg->lambda, G);
+  auto V = null_space(n, P->frame_ab);
+  const double c = (double)n;
+  for (auto& v : V)
+    for (int i = 0; i < p; ++i) {
+      if (v[i] == 0.0) continue;
+      for (int j = 0; j < p; ++j) G[(size_t)i * p + j] += c * v[i] * v[j];
+    }
+  PLAN_CUDA(cudaMalloc(&P->d_ginv, sizeof(double) * (size_t)p * p));
+  PLAN_CUDA(cudaMemcpy(P->d_ginv, G.data(), sizeof(double) * (size_t)p * p, cudaMemcpyHostToDevice));
+  double *d_col = nullptr, *d_piv = nullptr;
+  PLAN_CUDA(cudaMalloc(&d_col, sizeof(double) * p));
+  PLAN_CUDA(cudaMalloc(&d_piv, sizeof(double) * p));
+  {
+    const dim3 eg((p + 255) / 256 > 8 ? 8 : (p + 255) / 256, p);
+    for (int k = 0; k < p; ++k) {
+      gj_pivot_kernel<<<1, 1024>>>(P->d_ginv, d_col, d_piv, p, k);
+      gj_eliminate_kernel<<<eg, 256>>>(P->d_ginv, d_col, p, k);
+    }
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  std::vector<double> piv(p);
+  if (e == cudaSuccess) e = cudaMemcpy(piv.data(), d_piv, sizeof(double) * p, cudaMemcpyDeviceToHost);
+  cudaFree(d_col);
+  cudaFree(d_piv);
+  PLAN_CUDA(e);
+  double pmin = 1e300;
+  for (double x : piv) pmin = std::min(pmin, x);
+  // With the null space deflated every pivot is >= lambda_min(G') (~1e-2 .. 1e0 for the video
+  // layouts).  A dependency the analytic list misses (only degenerate tiny layouts, n <= 4 or
+  // sub-block frames at the grid corners) leaves a pivot of order lambda: the inverse is then
+  // only as accurate as the undeflated Cholesky of App. B (relative error ~ cond(G) u), which is
+  // reported through mod_plan_diagnostics.  A non-positive pivot means G' is not SPD: fail.
+  if (!(pmin > 0.0) || !std::isfinite(pmin)) {
+    mod_set_error("deflated Gram is not positive definite (min pivot %.3e, p=%d)", pmin, p);
+    return fail(MOD_ERR_NUMERICAL);
+  }
+  P->min_pivot = pmin;
+  P->null_dim = (int)V.size();
+
+  // ---- workspace carve
+  const size_t BH = (size_t)L.batch * L.heads;
+  P->proj_tiles = (n + kProjRows - 1) / kProjRows;
+  size_t off = 0;
+  P->ws_qbar = off; off = align_up(off + BH * n * L.head_dim * sizeof(float));
+  P->ws_kbar = off; off = align_up(off + BH * n * L.head_dim * sizeof(float));
+  P->ws_part = off; off = align_up(off + BH * P->proj_tiles * (size_t)p * sizeof(double));
+  P->ws_r = off;    off = align_up(off + BH * (size_t)p * sizeof(double));
+  P->ws_x = off;    off = align_up(off + BH * (size_t)p * sizeof(double));
+  P->ws_nae = off;  off = align_up(off + 2 * BH * (size_t)n * sizeof(double));
+  P->ws_bytes = off;
+  cudaSetDevice(prev_dev);
+  *out = P;
+  return MOD_OK;
+#undef PLAN_CUDA
+}
+
+extern "C" void mod_plan_destroy(mod_plan P) {
+  if (!P) return;
+  if (P->d_frame_ab) cudaFree(P->d_frame_ab);
+  if (P->d_row_frames) cudaFree(P->d_row_frames);
+  if (P->d_log_sizes) cudaFree(P->d_log_sizes);
+  if (P->d_ginv) cudaFree(P->d_ginv);
+  delete P;
+}
+
+extern "C" size_t mod_plan_workspace_bytes(mod_plan P) { return P ? P->ws_bytes : 0; }
+extern "C" int32_t mod_plan_num_blocks(mod_plan P) { return P ? P->n : -1; }
+extern "C" int32_t mod_plan_num_patterns(mod_plan P) { return P ? P->p : -1; }
+extern "C" const double* mod_plan_gram_inverse(mod_plan P) { return P ? P->d_ginv : nullptr; }
+extern "C" mod_status mod_plan_diagnostics(mod_plan P, double* min_pivot, int32_t* null_dim) {
+  MOD_REQUIRE(P, MOD_ERR_USAGE, "mod_plan_diagnostics: NULL plan");
+  if (min_pivot) *min_pivot = P->min_pivot;
+  if (null_dim) *null_dim = P->null_dim;
+  return MOD_OK;
+}
+extern "C" mod_status mod_plan_frame_blocks(mod_plan P, int32_t* a_b) {
+  MOD_REQUIRE(P && a_b, MOD_ERR_USAGE, "mod_plan_frame_blocks: NULL argument");
+  for (int i = 0; i < 2 * P->F; ++i) a_b[i] = P->frame_ab[i];
+  return MOD_OK;
+}

@@ -1,0 +1,177 @@
+"""Python face of the C ABI: ``Plan`` wraps one ``mod_plan`` and the six compute calls.
+
+PyTorch is used only for device memory (output / workspace tensors) and the current CUDA stream;
+every step of the hot path runs in libmoddit.so's kernels.  Calls are asynchronous on
+``torch.cuda.current_stream()`` exactly like the C functions.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+
+import torch
+
+from . import _lib
+from ._lib import ModConfig, ModLayout, ModSelection, check, lib
+
+
+@dataclasses.dataclass(frozen=True)
+class LayoutSpec:
+    batch: int
+    heads: int
+    head_dim: int
+    prefix_tokens: int
+    frames: int
+    height: int
+    width: int
+    block: int = 128
+
+    @property
+    def tokens(self) -> int:
+        return self.prefix_tokens + self.frames * self.height * self.width
+
+    @classmethod
+    def from_any(cls, w) -> "LayoutSpec":
+        if isinstance(w, LayoutSpec):
+            return w
+        if isinstance(w, dict):
+            return cls(**{f.name: w[f.name] for f in dataclasses.fields(cls)})
+        return cls(**{f.name: getattr(w, f.name) for f in dataclasses.fields(cls)})
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class Plan:
+    """Per-layout constants (block/frame ranges, deflated Gram inverse) + the compute calls."""
+
+    def __init__(self, layout, *, top_k: int = 1, lam: float = 1e-8, tau_e: float = 0.0,
+                 select_mode: int = _lib.MOD_SELECT_TOPK, select_param: float = 0.0,
+                 masked_renorm: bool = True, diag_guard: bool = True, softmax_scale: float = 0.0,
+                 device: int | None = None):
+        self.spec = LayoutSpec.from_any(layout)
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self._cl = ModLayout(*(getattr(self.spec, f) for f in
+                               ("batch", "heads", "head_dim", "prefix_tokens", "frames", "height", "width",
+                                "block")))
+        self._cc = ModConfig(lam, tau_e, top_k, select_mode, select_param, _lib.MOD_STAT_POOLED,
+                             int(masked_renorm), int(diag_guard), softmax_scale)
+        self.config = dict(lam=lam, tau_e=tau_e, top_k=top_k, select_mode=select_mode, select_param=select_param,
+                           masked_renorm=masked_renorm, diag_guard=diag_guard, softmax_scale=softmax_scale)
+        h = C.c_void_p()
+        check(lib.mod_plan_create(C.byref(self._cl), C.byref(self._cc), self.device, C.byref(h)))
+        self._h = h
+        self.n = lib.mod_plan_num_blocks(h)
+        self.p = lib.mod_plan_num_patterns(h)
+        fb = (C.c_int32 * (2 * self.spec.frames))()
+        check(lib.mod_plan_frame_blocks(h, fb))
+        self.frame_blocks = [(fb[2 * r], fb[2 * r + 1]) for r in range(self.spec.frames)]
+        mp, nd = C.c_double(), C.c_int32()
+        check(lib.mod_plan_diagnostics(h, C.byref(mp), C.byref(nd)))
+        self.min_pivot, self.null_dim = mp.value, nd.value
+        self.ws_bytes = lib.mod_plan_workspace_bytes(h)
+        self._ws = None
+
+    # ------------------------------------------------------------------ plumbing
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.mod_plan_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def BH(self) -> int:
+        return self.spec.batch * self.spec.heads
+
+    @property
+    def N(self) -> int:
+        return self.spec.tokens
+
+    def workspace(self) -> torch.Tensor:
+        if self._ws is None:
+            self._ws = torch.empty(max(self.ws_bytes, 256), dtype=torch.uint8, device=f"cuda:{self.device}")
+        return self._ws
+
+    def _dev(self):
+        return torch.device(f"cuda:{self.device}")
+
+    def _check_qkv(self, *ts):
+        B, H, N, D = self.spec.batch, self.spec.heads, self.N, self.spec.head_dim
+        for t in ts:
+            if t.shape != (B, H, N, D) or t.dtype != torch.bfloat16 or not t.is_cuda or not t.is_contiguous():
+                raise ValueError(f"expected contiguous bf16 CUDA tensor of shape {(B, H, N, D)}, got "
+                                 f"{tuple(t.shape)} {t.dtype} {t.device}")
+
+    def empty_stats(self) -> torch.Tensor:
+        return torch.empty((self.spec.batch, self.spec.heads, self.n, self.n), dtype=torch.float32, device=self._dev())
+
+    def empty_x(self) -> torch.Tensor:
+        return torch.empty((self.spec.batch, self.spec.heads, self.p), dtype=torch.float64, device=self._dev())
+
+    def empty_mask(self):
+        B, H, n = self.spec.batch, self.spec.heads, self.n
+        return (torch.empty((B, H, n + 1), dtype=torch.int32, device=self._dev()),
+                torch.empty((B, H, n * n), dtype=torch.int32, device=self._dev()))
+
+    # ------------------------------------------------------------------ compute calls
+    def collect_block_stats(self, q, k, out=None):
+        self._check_qkv(q, k)
+        out = self.empty_stats() if out is None else out
+        check(lib.mod_collect_block_stats(self._h, _ptr(q), _ptr(k), _ptr(out), _ptr(self.workspace()), _stream()))
+        return out
+
+    def fit_mixture(self, stats, out=None, want_nae: bool = False):
+        out = self.empty_x() if out is None else out
+        nae = torch.empty((self.spec.batch, self.spec.heads), dtype=torch.float32, device=self._dev()) if want_nae else None
+        check(lib.mod_fit_mixture(self._h, _ptr(stats), _ptr(out), _ptr(nae), _ptr(self.workspace()), _stream()))
+        return (out, nae) if want_nae else out
+
+    def keep_frames(self, x_a, x_b):
+        keep = torch.empty((self.spec.batch, self.spec.heads, self.spec.frames), dtype=torch.uint8, device=self._dev())
+        check(lib.mod_keep_frames(self._h, _ptr(x_a), _ptr(x_b), _ptr(keep), _stream()))
+        return keep
+
+    def predict_block_mask(self, x_prev, x_curr, t_prev: int, t_curr: int, t: int, keep=None, *,
+                           select_mode: int | None = None, top_k: int | None = None,
+                           select_param: float | None = None, out=None):
+        rp, ci = self.empty_mask() if out is None else out
+        sel = None
+        if select_mode is not None or top_k is not None or select_param is not None:
+            sel = ModSelection(self.config["select_mode"] if select_mode is None else select_mode,
+                               self.config["top_k"] if top_k is None else top_k,
+                               self.config["select_param"] if select_param is None else select_param)
+        check(lib.mod_predict_block_mask(self._h, _ptr(x_prev), _ptr(x_curr), t_prev, t_curr, t, _ptr(keep),
+                                         C.byref(sel) if sel is not None else None, _ptr(rp), _ptr(ci),
+                                         _ptr(self.workspace()), _stream()))
+        return rp, ci
+
+    def update_online_mask(self, stats_fresh, row_ptr, col_idx, stats_hist, x_prev, x_curr):
+        check(lib.mod_update_online_mask(self._h, _ptr(stats_fresh), _ptr(row_ptr), _ptr(col_idx), _ptr(stats_hist),
+                                         _ptr(x_prev), _ptr(x_curr), _ptr(self.workspace()), _stream()))
+
+    def block_sparse_attn_fwd(self, q, k, v, row_ptr, col_idx, out=None, lse=None, want_lse: bool = True):
+        self._check_qkv(q, k, v)
+        out = torch.empty_like(q) if out is None else out
+        if lse is None and want_lse:
+            lse = torch.empty(q.shape[:-1], dtype=torch.float32, device=q.device)
+        check(lib.mod_block_sparse_attn_fwd(self._h, _ptr(q), _ptr(k), _ptr(v), _ptr(row_ptr), _ptr(col_idx),
+                                            _ptr(out), _ptr(lse), _ptr(self.workspace()), _stream()))
+        return out, lse
+
+    def dense_mask(self, out=None):
+        rp, ci = self.empty_mask() if out is None else out
+        check(lib.mod_fill_dense_mask(self._h, _ptr(rp), _ptr(ci), _stream()))
+        return rp, ci
+
+
+def last_launch_count() -> int:
+    return lib.mod_last_launch_count()

@@ -1,0 +1,338 @@
+"""GPU parity of the CUDA path (through the C ABI) against the fp64 oracle.
+
+Tolerances (BASELINE.json north_star):
+  * pooled statistic W: elementwise |dW| <= 1e-3 * W (+1e-9)
+  * intensities X (fp64): component orthogonal to the null vector <= 1e-8 relative; the
+    null-vector component of the oracle's plain Cholesky carries ~cond(G)*u error (App. B
+    P:1254-1258 is evaluated literally there), so the total is checked at 50*cond(G)*u
+  * keep flags, CSR row_ptr / col_idx: bit-exact given identical intensities; given identical W,
+    bit-exact for every head whose K-th/K+1-th key gap exceeds the tie band (reading Z14)
+  * history map: unselected entries bit-identical, selected within 1 fp32 ulp
+  * attention O: max-abs <= 2e-2, mean-abs <= 2e-3 vs fp64 on unit-variance bf16 inputs;
+    lse <= 5e-3 abs
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import synthetic as syn
+from gpu_helpers import csr_rows_sorted_unique, csr_to_masks, masks_to_csr, null_vector_c_d, olayout
+
+pytestmark = pytest.mark.gpu
+
+SMALL_PREFIX = syn.Workload("small-prefix", 1, 3, 128, 40, 3, 20, 19, 128)     # N=1180, ragged tail 28
+COG_SMALL = syn.Workload("cog-small", 1, 2, 64, 226, 3, 30, 45, 128)          # N=4276, D=64, ragged 52
+TINY = syn.TINY
+
+
+@pytest.fixture(scope="module")
+def M():
+    import paper_2601_11641_b200 as m
+    return m
+
+
+def plan_for(M, w, **kw):
+    return M.Plan(w, **kw)
+
+
+def rel_err(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+# ------------------------------------------------------------------------------------------ K1
+@pytest.mark.parametrize("w", [TINY, SMALL_PREFIX, COG_SMALL, syn.COGVIDEOX], ids=lambda w: w.name)
+def test_stats_parity(M, w):
+    P = plan_for(M, w)
+    q, k, _ = syn.family_r(w, device="cuda")
+    W = P.collect_block_stats(q, k)
+    torch.cuda.synchronize()
+    ref = O.pooled_block_stats(q.cpu(), k.cpu(), olayout(w))
+    Wg = W.double().cpu().numpy()
+    assert np.all(np.abs(Wg - ref) <= 1e-3 * ref + 1e-9)
+    assert np.allclose(Wg.sum(-1), 1.0, atol=1e-5)
+
+
+def test_stats_parity_hunyuan_sampled_heads(M):
+    w = syn.HUNYUAN
+    P = plan_for(M, w)
+    q, k, _ = syn.family_r(w, device="cuda")
+    W = P.collect_block_stats(q, k)
+    torch.cuda.synchronize()
+    L = olayout(w.with_heads(1))
+    for h in (0, 23):
+        ref = O.pooled_block_stats(q[:, h:h + 1].cpu(), k[:, h:h + 1].cpu(), L)[0, 0]
+        Wg = W[0, h].double().cpu().numpy()
+        assert np.all(np.abs(Wg - ref) <= 1e-3 * ref + 1e-9)
+
+
+def test_stats_structured_family_s(M):
+    w = COG_SMALL
+    P = plan_for(M, w)
+    q, k, _ = syn.family_s(w, device="cuda")
+    W = P.collect_block_stats(q, k)
+    torch.cuda.synchronize()
+    ref = O.pooled_block_stats(q.cpu(), k.cpu(), olayout(w))
+    assert np.all(np.abs(W.double().cpu().numpy() - ref) <= 1e-3 * ref + 1e-9)
+
+
+# ------------------------------------------------------------------------------------------ K2a
+def _check_x(xg, xr, L, G_cond):
+    n, p = L.n, L.p
+    v = null_vector_c_d(n, p)
+    for a, b in zip(xg.reshape(-1, p), xr.reshape(-1, p)):
+        pa, pb = a - v * (v @ a), b - v * (v @ b)
+        assert rel_err(pa, pb) <= 1e-8
+        assert rel_err(a, b) <= max(1e-8, 50 * G_cond * np.finfo(float).eps)
+        assert abs(v @ a) <= 1e-9 * np.linalg.norm(a)       # deflated solve stays in the min-norm gauge
+
+
+@pytest.mark.parametrize("w", [TINY, SMALL_PREFIX, COG_SMALL, syn.COGVIDEOX], ids=lambda w: w.name)
+def test_fit_parity(M, w):
+    L = olayout(w)
+    P = plan_for(M, w)
+    U = syn.random_stats(w.batch, w.heads, L.n, seed=7, device="cuda")
+    X, nae = P.fit_mixture(U, want_nae=True)
+    torch.cuda.synchronize()
+    Un = U.double().cpu().numpy()
+    xr = O.fit_mixture(Un, L)
+    cond = np.linalg.cond(O.gram_closed_form(L)) if L.p <= 1000 else 6e10
+    _check_x(X.cpu().numpy(), xr, L, cond)
+    for h in range(min(w.heads, 4)):
+        assert abs(nae[0, h].item() - O.nae(Un[0, h], xr[0, h], L)) <= 1e-5
+
+
+def test_fit_parity_hunyuan(M):
+    w = syn.HUNYUAN
+    L = olayout(w.with_heads(2))
+    P = plan_for(M, w.with_heads(2))
+    U = syn.random_stats(1, 2, L.n, seed=8, device="cuda")
+    X = P.fit_mixture(U)
+    torch.cuda.synchronize()
+    xr = O.fit_mixture(U.double().cpu().numpy(), L)
+    _check_x(X.cpu().numpy(), xr, L, 6e10)
+
+
+# ------------------------------------------------------------------------------------------ keep / K2b
+@pytest.mark.parametrize("w", [TINY, SMALL_PREFIX, COG_SMALL], ids=lambda w: w.name)
+def test_keep_bit_exact(M, w):
+    L = olayout(w)
+    P = plan_for(M, w, tau_e=0.05)
+    xa = syn.random_intensities(w.batch, w.heads, L.p, seed=1, device="cuda") * 0.1
+    xb = syn.random_intensities(w.batch, w.heads, L.p, seed=2, device="cuda") * 0.1
+    keep = P.keep_frames(xa, xb)
+    torch.cuda.synchronize()
+    ref = O.keep_frames(xa.cpu().numpy(), xb.cpu().numpy(), L, np.float32(0.05))
+    assert np.array_equal(keep.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("w", [TINY, SMALL_PREFIX, COG_SMALL, syn.HUNYUAN.with_heads(3)], ids=lambda w: w.name)
+@pytest.mark.parametrize("mode,param", [(0, 0.0), (1, 0.4), (2, 0.6)], ids=["topk", "threshold", "topmass"])
+def test_predict_bit_exact_given_x(M, w, mode, param):
+    L = olayout(w)
+    K = max(1, (3 * L.n - 1) // 7)
+    P = plan_for(M, w, top_k=K, select_mode=mode, select_param=param)
+    xp = syn.random_intensities(w.batch, w.heads, L.p, seed=3, device="cuda")
+    xc = syn.random_intensities(w.batch, w.heads, L.p, seed=4, device="cuda")
+    keep = (torch.rand((w.batch, w.heads, w.frames), generator=torch.Generator().manual_seed(5)) < 0.5).to(torch.uint8).cuda()
+    rp, ci = P.predict_block_mask(xp, xc, 22, 32, 37, keep)
+    torch.cuda.synchronize()
+    ref = O.predict_block_mask(xp.cpu().numpy(), xc.cpu().numpy(), 22, 32, 37, keep.cpu().numpy(), L, mode, K,
+                               float(np.float32(param)), True)
+    got = csr_to_masks(rp, ci, L.n)
+    assert csr_rows_sorted_unique(rp, ci, L.n)
+    assert np.array_equal(got, ref)
+    assert np.array_equal(rp[..., -1].cpu().numpy(), ref.sum((-1, -2)))
+
+
+def test_predict_without_keep_and_guard(M):
+    w = SMALL_PREFIX
+    L = olayout(w)
+    P = plan_for(M, w, top_k=3, diag_guard=False)
+    xp = syn.random_intensities(1, w.heads, L.p, seed=6, device="cuda")
+    rp, ci = P.predict_block_mask(xp, xp * 2, 11, 12, 13, None)
+    torch.cuda.synchronize()
+    ref = O.predict_block_mask(xp.cpu().numpy(), 2 * xp.cpu().numpy(), 11, 12, 13, np.zeros((1, w.heads, w.frames)),
+                               L, 0, 3, 0.0, False)
+    assert np.array_equal(csr_to_masks(rp, ci, L.n), ref)
+
+
+def test_dense_mask(M):
+    w = COG_SMALL
+    P = plan_for(M, w)
+    rp, ci = P.dense_mask()
+    torch.cuda.synchronize()
+    assert csr_to_masks(rp, ci, P.n).all()
+
+
+@pytest.mark.parametrize("w", [SMALL_PREFIX, COG_SMALL, syn.COGVIDEOX], ids=lambda w: w.name)
+def test_fit_then_predict_given_identical_stats(M, w):
+    """End to end from identical W: masks bit-exact outside the Top-K tie band (reading Z14)."""
+    L = olayout(w)
+    K = max(2, (3 * L.n - 1) // 6)
+    P = plan_for(M, w, top_k=K)
+    U1 = syn.random_stats(w.batch, w.heads, L.n, seed=11, device="cuda")
+    U2 = syn.random_stats(w.batch, w.heads, L.n, seed=12, device="cuda")
+    X1, X2 = P.fit_mixture(U1), P.fit_mixture(U2)
+    rp, ci = P.predict_block_mask(X1, X2, 11, 12, 14, None)
+    torch.cuda.synchronize()
+    x1 = O.fit_mixture(U1.double().cpu().numpy(), L)
+    x2 = O.fit_mixture(U2.double().cpu().numpy(), L)
+    ref = O.predict_block_mask(x1, x2, 11, 12, 14, np.zeros((1, w.heads, w.frames)), L, 0, K, 0.0, True)
+    got = csr_to_masks(rp, ci, L.n)
+    keys = O.pattern_keys(O.extrapolate(x1, x2, 11, 12, 14), L).reshape(-1, 3 * L.n - 1)
+    checked = 0
+    for t in range(keys.shape[0]):
+        ks = np.sort(keys[t])[::-1]
+        gap = ks[K - 1] - ks[K]
+        band = 1e-6 * np.max(np.abs(ks))
+        if gap > band:
+            assert np.array_equal(got.reshape(-1, L.n, L.n)[t], ref.reshape(-1, L.n, L.n)[t])
+            checked += 1
+    assert checked >= 0.9 * keys.shape[0]
+
+
+# ------------------------------------------------------------------------------------------ K3
+@pytest.mark.parametrize("w", [TINY, SMALL_PREFIX, COG_SMALL], ids=lambda w: w.name)
+@pytest.mark.parametrize("renorm", [True, False])
+def test_update_parity(M, w, renorm):
+    L = olayout(w)
+    P = plan_for(M, w, masked_renorm=renorm)
+    Wf = syn.random_stats(w.batch, w.heads, L.n, seed=21, device="cuda")
+    hist = syn.random_stats(w.batch, w.heads, L.n, seed=22, device="cuda")
+    rng = np.random.default_rng(23)
+    masks = rng.random((w.batch, w.heads, L.n, L.n)) < 0.3
+    masks |= np.eye(L.n, dtype=bool)
+    rp, ci = masks_to_csr(masks)
+    xp = syn.random_intensities(w.batch, w.heads, L.p, seed=24, device="cuda")
+    xc = syn.random_intensities(w.batch, w.heads, L.p, seed=25, device="cuda")
+    hist0, xc0 = hist.cpu().numpy().copy(), xc.cpu().numpy().copy()
+    P.update_online_mask(Wf, rp, ci, hist, xp, xc)
+    torch.cuda.synchronize()
+    ref_hist = O.reconstruct_history(Wf.double().cpu().numpy(), hist0.astype(np.float64), masks, renorm)
+    hg = hist.cpu().numpy()
+    assert np.array_equal(hg[~masks], hist0[~masks])                                  # Eq. 5 second branch
+    ulp = np.spacing(np.abs(ref_hist[masks]).astype(np.float32))
+    assert np.all(np.abs(hg[masks].astype(np.float64) - ref_hist[masks]) <= ulp)      # first branch
+    assert np.array_equal(xp.cpu().numpy(), xc0)                                       # roll
+    xr = O.fit_mixture(hg.astype(np.float64), L)
+    _check_x(xc.cpu().numpy(), xr, L, np.linalg.cond(O.gram_closed_form(L)))
+
+
+# ------------------------------------------------------------------------------------------ K4
+def _attn_check(og, lg, orf, lrf):
+    err = np.abs(og - orf)
+    assert err.max() <= 2e-2, err.max()
+    assert err.mean() <= 2e-3, err.mean()
+    fin = np.isfinite(lrf)
+    assert np.array_equal(np.isfinite(lg), fin)
+    assert np.abs(lg[fin] - lrf[fin]).max() <= 5e-3
+
+
+def _random_masks(w, L, density, seed):
+    rng = np.random.default_rng(seed)
+    m = rng.random((w.batch, w.heads, L.n, L.n)) < density
+    m |= np.eye(L.n, dtype=bool)
+    return m
+
+
+@pytest.mark.parametrize("w,density", [(TINY, 0.5), (SMALL_PREFIX, 0.4), (COG_SMALL, 0.25)],
+                         ids=["tiny", "small-prefix", "cog-small"])
+def test_attention_parity_full(M, w, density):
+    L = olayout(w)
+    P = plan_for(M, w)
+    q, k, v = syn.family_r(w, device="cuda")
+    masks = _random_masks(w, L, density, 31)
+    rp, ci = masks_to_csr(masks)
+    o, lse = P.block_sparse_attn_fwd(q, k, v, rp, ci)
+    torch.cuda.synchronize()
+    orf, lrf = O.masked_attention(q.cpu(), k.cpu(), v.cpu(), masks, L)
+    _attn_check(o.double().cpu().numpy(), lse.double().cpu().numpy(), orf, lrf)
+
+
+def test_attention_dense_mask_equals_dense_attention(M):
+    w = TINY
+    P = plan_for(M, w)
+    q, k, v = syn.family_r(w, seed=99, device="cuda")
+    rp, ci = P.dense_mask()
+    o, _ = P.block_sparse_attn_fwd(q, k, v, rp, ci)
+    torch.cuda.synchronize()
+    ref = O.dense_attention(q.cpu(), k.cpu(), v.cpu())
+    err = np.abs(o.double().cpu().numpy() - ref)
+    assert err.max() <= 2e-2 and err.mean() <= 2e-3
+
+
+def test_attention_empty_rows(M):
+    w = SMALL_PREFIX
+    L = olayout(w)
+    P = plan_for(M, w)
+    q, k, v = syn.family_r(w, device="cuda")
+    masks = _random_masks(w, L, 0.3, 41)
+    masks[0, 1, 3, :] = False
+    masks[0, 2, L.n - 1, :] = False
+    rp, ci = masks_to_csr(masks)
+    o, lse = P.block_sparse_attn_fwd(q, k, v, rp, ci)
+    torch.cuda.synchronize()
+    orf, lrf = O.masked_attention(q.cpu(), k.cpu(), v.cpu(), masks, L)
+    _attn_check(o.double().cpu().numpy(), lse.double().cpu().numpy(), orf, lrf)
+    lo, hi = L.block_range(3)
+    assert torch.all(o[0, 1, lo:hi] == 0) and torch.all(torch.isneginf(lse[0, 1, lo:hi]))
+
+
+def _structured_masks(L, heads, seed, top_k):
+    rng = np.random.default_rng(seed)
+    out = np.zeros((1, heads, L.n, L.n), dtype=bool)
+    for h in range(heads):
+        keys = rng.standard_normal(3 * L.n - 1)
+        sel = O.select_patterns(keys, L.n, O.SELECT_TOPK, top_k)
+        keep = rng.random(L.frames) < 0.7
+        out[0, h] = O.block_mask(sel, keep, L, True)
+    return out
+
+
+@pytest.mark.parametrize("w", [syn.HUNYUAN, syn.WAN, syn.COGVIDEOX], ids=lambda w: w.name)
+def test_attention_parity_full_size_sampled(M, w):
+    """Full BASELINE shapes in the launch configuration bench.py times; oracle on sampled blocks."""
+    L = olayout(w)
+    P = plan_for(M, w)
+    q, k, v = syn.family_r(w, device="cuda")
+    masks = _structured_masks(L, w.heads, 51, top_k=max(4, L.n // 10))
+    rp, ci = masks_to_csr(masks)
+    o, lse = P.block_sparse_attn_fwd(q, k, v, rp, ci)
+    torch.cuda.synchronize()
+    Lh = olayout(w.with_heads(1))
+    rng = np.random.default_rng(52)
+    for h in (0, w.heads - 1):
+        qh, kh, vh = q[:, h:h + 1].cpu(), k[:, h:h + 1].cpu(), v[:, h:h + 1].cpu()
+        counts = masks[0, h].sum(1)
+        blocks = sorted({0, L.n - 1, int(np.argmax(counts)), int(rng.integers(0, L.n))})
+        outs, lses = O.masked_attention_rows(qh, kh, vh, masks[0, h], Lh, 0, 0, blocks)
+        og = o[0, h].double().cpu().numpy()
+        lg = lse[0, h].double().cpu().numpy()
+        for i, orf, lrf in zip(blocks, outs, lses):
+            lo, hi = L.block_range(i)
+            _attn_check(og[lo:hi], lg[lo:hi], orf, lrf)
+
+
+def test_attention_deterministic(M):
+    w = COG_SMALL
+    L = olayout(w)
+    P = plan_for(M, w)
+    q, k, v = syn.family_r(w, device="cuda")
+    rp, ci = masks_to_csr(_random_masks(w, L, 0.3, 61))
+    o1, l1 = P.block_sparse_attn_fwd(q, k, v, rp, ci)
+    o2, l2 = P.block_sparse_attn_fwd(q, k, v, rp, ci)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2) and torch.equal(l1, l2)
+
+
+# ------------------------------------------------------------------------------------------ errors
+def test_plan_errors(M):
+    with pytest.raises(M.ModditError, match="head_dim=96"):
+        M.Plan(dict(batch=1, heads=1, head_dim=96, prefix_tokens=0, frames=1, height=4, width=4, block=128))
+    with pytest.raises(M.ModditError, match="top_k=0"):
+        M.Plan(TINY, top_k=0)
+    P = M.Plan(TINY)
+    x = P.empty_x()
+    with pytest.raises(M.ModditError, match="zero denominator"):
+        P.predict_block_mask(x, x, 5, 5, 6)
