@@ -1,0 +1,455 @@
+#!/usr/bin/env python
+"""bench.py -- MOD-DiT hot path on B200: block-sparse attention fwd (ms, TFLOPS, % of bf16 peak) vs dense
+at the HunyuanVideo 720p shape (BASELINE.json "metric", configs[3]).
+
+One STEP = one pass of the whole hot path of SURVEY.md 8(a) at a re-estimation step t_p of
+Algorithm 1, on synthetic Family-S inputs resident in HBM:
+    K2b mod_predict_block_mask   (Eq. 6/7 + Top-K + CSR)        -> mask for step t
+    K4  mod_block_sparse_attn_fwd (Eq. 1 over the index lists)   -> O, lse
+    K1  mod_collect_block_stats  (pooled block statistic)       -> fresh W
+    K3  mod_update_online_mask   (Eq. 5 + refit (K2a) + roll)
+The warm-up (two pooled statistics + fits, keep decision) runs once before timing; K is bisected
+so that the mean block sparsity hits --sparsity (default 0.878, the paper's HunyuanVideo
+sparsity, Table 1).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config hunyuan]
+Multi-GPU (torchrun): heads are partitioned across ranks (no data-path collective; head-parallel,
+SURVEY 8(e)); value = all ranks' attention FLOPs / max-over-ranks time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synthetic as syn  # noqa: E402
+
+M_WARMUP, DT, T_TOTAL = 12, 10, 50          # Alg. 1 defaults: m = 12, Delta t = 10, T = 50
+METRIC = "block-sparse attn fwd ms & TFLOPS (% bf16 peak) vs dense at HunyuanVideo shape"
+
+
+def attn_flops(row_ptr: np.ndarray, col_idx: np.ndarray, N: int, block: int, D: int) -> float:
+    """Algorithmic FLOPs of K4: 4 * D * sum over selected (i,j) of |I_i| * |I_j| (QK^T + PV)."""
+    n = row_ptr.shape[-1] - 1
+    sizes = np.minimum((np.arange(n) + 1) * block, N) - np.arange(n) * block
+    tot = 0
+    for rp, ci in zip(row_ptr.reshape(-1, n + 1), col_idx.reshape(-1, col_idx.shape[-1])):
+        nnz = rp[-1]
+        rows = np.repeat(np.arange(n), np.diff(rp))
+        tot += int(np.dot(sizes[rows], sizes[ci[:nnz]]))
+    return 4.0 * D * tot
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return d["bf16_tflops"], d.get("bf16_tflops_sustained", d["bf16_tflops"]), d["hbm_gbs"], "measured"
+    except Exception:
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index: int):
+        self.index, self.samples, self._stop = index, [], threading.Event()
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 2 + i and "Active" in s[2 + i]
+                          and "Not" not in s[2 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons}
+
+
+# ---------------------------------------------------------------------------------------- distributed
+def dist_setup(n_gpus: int):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    else:
+        torch.cuda.set_device(0)
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, ws: int) -> float:
+    if ws == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x: float, ws: int) -> float:
+    if ws == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------------------- our arm
+def bisect_top_k(P, x_prev, x_curr, keep, target_sparsity: float, ws: int):
+    """Smallest K whose mean block sparsity (over all ranks' heads) is <= target (reading Z8)."""
+    n = P.n
+    lo, hi = 1, 3 * n - 1
+
+    def sparsity(K):
+        rp, _ = P.predict_block_mask(x_prev, x_curr, M_WARMUP - 1, M_WARMUP, M_WARMUP + DT, keep, top_k=K)
+        nnz = sum_over_ranks(float(rp[..., -1].sum().item()), ws)
+        return 1.0 - nnz / (P.BH * ws * n * n)
+
+    while lo < hi:
+        mid = (lo + hi) // 2
+        if sparsity(mid) <= target_sparsity:
+            hi = mid
+        else:
+            lo = mid + 1
+    return lo, sparsity(lo)
+
+
+def dense_reference_ms(q, k, v, reps: int = 3):
+    """Fastest dense attention available on the box (library comparators; context only)."""
+    import torch.nn.functional as F
+    from torch.nn.attention import SDPBackend, sdpa_kernel
+    res = {}
+    for name, be in (("cudnn", SDPBackend.CUDNN_ATTENTION), ("flash", SDPBackend.FLASH_ATTENTION)):
+        try:
+            with sdpa_kernel(be):
+                F.scaled_dot_product_attention(q, k, v)
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(reps):
+                    F.scaled_dot_product_attention(q, k, v)
+                e1.record()
+                torch.cuda.synchronize()
+                res[name] = e0.elapsed_time(e1) / reps
+        except Exception as ex:  # backend unavailable for this shape
+            res[name] = None
+            res[name + "_error"] = str(ex)[:120]
+    return res
+
+
+def run_ours(args):
+    import paper_2601_11641_b200 as mod
+    from paper_2601_11641_b200 import Plan
+
+    ws, rank, local = dist_setup(args.gpus)
+    w_full = syn.CONFIGS[args.config]
+    assert w_full.heads % ws == 0, f"heads {w_full.heads} not divisible by {ws} ranks"
+    Hl = w_full.heads // ws
+    h0 = rank * Hl
+    w = w_full.with_heads(Hl)
+    D, N, blk = w.head_dim, w.tokens, w.block
+    burst, sustained, hbm, peak_src = load_peaks()
+
+    P = Plan(w, top_k=1, tau_e=0.0)
+    gen = dict(seed=syn.SEED_BASE, device="cuda", head_offset=h0, total_heads=w_full.heads)
+    # ---- warm-up phase of Alg. 1: statistics at t = m-1 and t = m, fits, keep decision
+    q1, k1, _ = syn.family_s(w, step=M_WARMUP - 1, **gen)
+    W1 = P.collect_block_stats(q1, k1)
+    del q1, k1
+    q, k, v = syn.family_s(w, step=M_WARMUP, **gen)
+    W2 = P.collect_block_stats(q, k)
+    x_prev0, x_curr0 = P.fit_mixture(W1), P.fit_mixture(W2)
+    keep = P.keep_frames(x_prev0, x_curr0)
+    hist = W2.clone()                                  # A_hat^(t_p^(0)) = A^(m)
+    K, sp = bisect_top_k(P, x_prev0, x_curr0, keep, args.sparsity, ws)
+    t_step = M_WARMUP + DT                             # t_p^(1) = 22
+    xs_prev, xs_curr = x_prev0.clone(), x_curr0.clone()
+    rp, ci = P.empty_mask()
+    o = torch.empty_like(q)
+    lse = torch.empty(q.shape[:-1], dtype=torch.float32, device="cuda")
+    Wf = P.empty_stats()
+    stream = torch.cuda.current_stream()
+    ev = {k_: [] for k_ in ("attn", "rest")}
+
+    def step(timed_kernels=False):
+        if timed_kernels:
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            e[0].record(stream)
+        P.predict_block_mask(x_prev0, x_curr0, M_WARMUP - 1, M_WARMUP, t_step, keep, top_k=K, out=(rp, ci))
+        if timed_kernels:
+            e[1].record(stream)
+        P.block_sparse_attn_fwd(q, k, v, rp, ci, out=o, lse=lse)
+        if timed_kernels:
+            e[2].record(stream)
+        P.collect_block_stats(q, k, out=Wf)
+        P.update_online_mask(Wf, rp, ci, hist, xs_prev, xs_curr)
+        if timed_kernels:
+            e[3].record(stream)
+            ev["attn"].append((e[1], e[2]))
+            ev["rest"].append((e[0], e[1], e[2], e[3]))
+
+    launches_per_step = 1 + 1 + 2 + 5
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    rpn, cin = rp.cpu().numpy(), ci.cpu().numpy()
+    flops_local = attn_flops(rpn, cin, N, blk, D)
+    flops_all = sum_over_ranks(flops_local, ws)
+    nnz_local = float(rpn[..., -1].sum())
+
+    # ---- timed region: K steps, barrier + sync on both sides, CUDA events, max over ranks
+    barrier(ws)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step(timed_kernels=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier(ws)
+    ms_local = e0.elapsed_time(e1) / args.steps
+    ms = max_over_ranks(ms_local, ws)
+    attn_ms = statistics.mean(a.elapsed_time(b) for a, b in ev["attn"])
+    pred_ms = statistics.mean(a.elapsed_time(b) for a, b, _, _ in ev["rest"])
+    upd_ms = statistics.mean(c.elapsed_time(d) for _, _, c, d in ev["rest"])
+    attn_ms_max = max_over_ranks(attn_ms, ws)
+    value = flops_all / (ms * 1e-3) / 1e12
+    attn_tflops = flops_local / (attn_ms * 1e-3) / 1e12
+
+    out = {"metric": METRIC, "value": round(value, 2), "unit": "TFLOPS", "n_gpus": ws, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "bf16", "data": "synthetic (Family S, seeded; SURVEY 8(d))"}
+
+    # ---- dense comparators (rank 0, 1 GPU shape of its heads): library SDPA + our K4 with all-ones CSR
+    dense = {}
+    if rank == 0 and not args.no_dense:
+        dense = dense_reference_ms(q, k, v)
+        rpd, cid = P.dense_mask()
+        P.block_sparse_attn_fwd(q, k, v, rpd, cid, out=o, lse=lse)
+        torch.cuda.synchronize()
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d0.record()
+        for _ in range(2):
+            P.block_sparse_attn_fwd(q, k, v, rpd, cid, out=o, lse=lse)
+        d1.record()
+        torch.cuda.synchronize()
+        dense["ours_all_ones_csr"] = d0.elapsed_time(d1) / 2
+        del rpd, cid
+    dense_flops = 4.0 * D * N * N * w.batch * w.heads
+    fastest = min([x for kk, x in dense.items() if isinstance(x, float)], default=None)
+
+    # ---- e2e through the public API with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
+        ho = torch.empty_like(hq).pin_memory()
+        barrier(ws)
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(args.steps):
+            q.copy_(hq, non_blocking=True)
+            k.copy_(hk, non_blocking=True)
+            v.copy_(hv, non_blocking=True)
+            step()
+            ho.copy_(o, non_blocking=True)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = max_over_ranks(s0.elapsed_time(s1) / args.steps, ws)
+        e2e = {"value": round(flops_all / (e2e_ms * 1e-3) / 1e12, 2), "unit": "TFLOPS",
+               "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": int(3 * q.numel() * 2 * ws),
+               "d2h_bytes_per_step": int(o.numel() * 2 * ws)}
+        del hq, hk, hv, ho
+
+    # ---- roofline of the dominant kernel (K4): algorithmic FLOPs / event-timed launch duration
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "k4_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(args.config)
+        except Exception:
+            traffic = None
+    roof = {"bound": "tensor", "achieved": round(attn_tflops, 1), "peak": burst, "unit": "TFLOP/s",
+            "frac": round(attn_tflops / burst, 4), "frac_of_sustained": round(attn_tflops / sustained, 4),
+            "peak_source": peak_src, "traffic": traffic, "kernel": "attn_fwd_kernel<128,128>",
+            "algorithmic_flops_per_launch": flops_local}
+
+    out.update({
+        "config": {"workload": f"{w_full.name}: B={w_full.batch} H={w_full.heads} D={D} N={N} "
+                               f"({w_full.frames}x{w_full.height}x{w_full.width}+{w_full.prefix_tokens}), block {blk}",
+                   "heads_per_rank": Hl, "top_k": K, "block_sparsity": round(sp, 4),
+                   "target_sparsity": args.sparsity, "nnz_blocks_rank0": nnz_local,
+                   "step": "predict(K2b) + attn(K4) + stats(K1) + update(K3: Eq.5 + fit K2a + roll) at t_p=22",
+                   "l2": "inputs larger than L2 (Q,K,V = %.2f GB per rank > 126 MB)" % (3 * q.numel() * 2 / 1e9),
+                   "parallelism": f"head-parallel x{ws}"},
+        "attn_ms": round(attn_ms_max, 3), "attn_tflops": round(attn_tflops, 1),
+        "attn_pct_bf16_peak": round(100 * attn_tflops / burst, 1),
+        "pipeline_overhead_ms": {"predict": round(pred_ms, 4), "stats_update": round(upd_ms, 4)},
+        "dense_ms": {kk: (round(x, 3) if isinstance(x, float) else x) for kk, x in dense.items()},
+        "dense_tflops_fastest": round(dense_flops / (fastest * 1e-3) / 1e12, 1) if fastest else None,
+        "speedup_vs_fastest_dense": round(fastest / attn_ms, 3) if fastest else None,
+        "roofline": roof, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
+        "clocks": clk.summary(), "library": mod.LIB_PATH,
+    })
+
+    # ---- cpu baseline: the oracle as it stands on a bounded sample (rank 0, N=1 only)
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        out["cpu_baseline"] = cpu_baseline(w, q, k, v, rpn, cin, args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def cpu_baseline(w, q, k, v, rpn, cin, budget_s: float):
+    """Oracle masked attention on sampled query blocks of head 0 (same mask), timed on host cores."""
+    import oracle as O
+    L = O.make_layout(1, 1, w.head_dim, w.prefix_tokens, w.frames, w.height, w.width, w.block)
+    mask = O.csr_to_mask(rpn[0, 0], cin[0, 0], L.n)
+    qh, kh, vh = (t[:, :1].cpu() for t in (q, k, v))
+    rng = np.random.default_rng(0)
+    order = rng.permutation(L.n)
+    t0 = time.perf_counter()
+    flops, nb = 0.0, 0
+    for i in order:
+        O.masked_attention_rows(qh, kh, vh, mask, L, 0, 0, [int(i)])
+        lo, hi = L.block_range(int(i))
+        keys = sum(L.block_size(j) for j in np.nonzero(mask[i])[0])
+        flops += 4.0 * w.head_dim * (hi - lo) * keys
+        nb += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": flops / dt / 1e12, "unit": "TFLOPS", "cores": os.cpu_count(), "kind": "oracle",
+            "sample": f"{nb} query blocks of head 0 (oracle masked_attention_rows, fp64 numpy, same mask), "
+                      f"{dt:.1f} s", "threads": torch.get_num_threads()}
+
+
+# ---------------------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    """The oracle timed on the host cores (the 'reference' of this tier), bounded sample per step."""
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle as O
+    w = syn.CONFIGS[args.config].with_heads(1)
+    L = O.make_layout(1, 1, w.head_dim, w.prefix_tokens, w.frames, w.height, w.width, w.block)
+    gen = dict(seed=syn.SEED_BASE, device="cpu", total_heads=syn.CONFIGS[args.config].heads)
+    q1, k1, _ = syn.family_s(w, step=M_WARMUP - 1, **gen)
+    q, k, v = syn.family_s(w, step=M_WARMUP, **gen)
+    W1 = O.pooled_block_stats(q1, k1, L)
+    W2 = O.pooled_block_stats(q, k, L)
+    x1, x2 = O.fit_mixture(W1, L), O.fit_mixture(W2, L)
+    keep = O.keep_frames(x1, x2, L, 0.0)
+    n = L.n
+    lo, hi = 1, 3 * n - 1
+    while lo < hi:                                     # same K rule as our arm, evaluated by the oracle
+        mid = (lo + hi) // 2
+        m_ = O.predict_block_mask(x1, x2, M_WARMUP - 1, M_WARMUP, M_WARMUP + DT, keep, L, O.SELECT_TOPK, mid)
+        if 1.0 - m_.mean() <= args.sparsity:
+            hi = mid
+        else:
+            lo = mid + 1
+    K = lo
+    rng = np.random.default_rng(0)
+    sample_blocks = int(args.ref_blocks)
+
+    def step():
+        masks = O.predict_block_mask(x1, x2, M_WARMUP - 1, M_WARMUP, M_WARMUP + DT, keep, L, O.SELECT_TOPK, K)
+        blocks = rng.choice(n, size=sample_blocks, replace=False)
+        O.masked_attention_rows(q, k, v, masks[0, 0], L, 0, 0, [int(b) for b in blocks])
+        fl = sum(4.0 * w.head_dim * L.block_size(int(i)) * sum(L.block_size(j) for j in np.nonzero(masks[0, 0, i])[0])
+                 for i in blocks)
+        return fl
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    fl = 0.0
+    for _ in range(args.steps):
+        fl += step()
+    dt = time.perf_counter() - t0
+    val = fl / dt / 1e12
+    out = {"metric": METRIC, "value": val, "unit": "TFLOPS", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+           "dtype": "f64", "data": "synthetic (Family S, seeded)", "impl": "reference",
+           "config": {"workload": f"{syn.CONFIGS[args.config].name} (oracle sample: head 0, {sample_blocks} query "
+                                  f"blocks per step)", "top_k": K},
+           "cpu_baseline": {"value": val, "unit": "TFLOPS", "cores": os.cpu_count(), "kind": "oracle",
+                            "sample": f"{sample_blocks} random query blocks of head 0 per step"},
+           "e2e": {"value": val, "unit": "TFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="hunyuanvideo-720p", choices=sorted(syn.CONFIGS))
+    ap.add_argument("--sparsity", type=float, default=0.878)
+    ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-blocks", type=int, default=4)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

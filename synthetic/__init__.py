@@ -73,7 +73,8 @@ def family_r(w: Workload, seed: int = SEED_BASE, device="cpu"):
 
 
 def family_s(w: Workload, seed: int = SEED_BASE, device="cpu", sigma: float = 0.5,
-             kappa: float = 1.0, n_random_sinks: int = 2):
+             kappa: float = 1.0, n_random_sinks: int = 2, step: int = 0, head_offset: int = 0,
+             total_heads: int | None = None):
     """Family S (structured): planted intra-frame, inter-frame and global-column structure.
 
     Q = a_h*phi(y,x) + b_h*psi(f) + c_h*g_h + sigma*eps
@@ -82,22 +83,26 @@ def family_s(w: Workload, seed: int = SEED_BASE, device="cpu", sigma: float = 0.
     (a_h, b_h, c_h) ~ Dirichlet(1,1,1)*scale per head; sinks = block 0 plus
     ``n_random_sinks`` seeded random blocks per head; V ~ N(0, 1).  Each tensor is
     rescaled to unit per-element variance, then rounded to bf16.
+    ``step`` re-draws only the noise eps (emulates consecutive denoising steps with the same
+    structure).  ``head_offset``/``total_heads`` generate the heads [head_offset, head_offset+H) of a
+    ``total_heads``-head problem (head-parallel ranks draw exactly the bytes a single GPU would).
     """
     B, H, N, D = w.batch, w.heads, w.tokens, w.head_dim
+    HT = total_heads or H
     g = _gen(seed, "cpu")
     # small per-head / per-frame parameters are drawn on the CPU (cheap, device independent)
     dirich = torch.distributions.Dirichlet(torch.ones(3))
     torch.manual_seed(seed)  # Dirichlet uses the global generator; seed it for determinism
-    abc = dirich.sample((H,)) * 2.0                                     # [H, 3]
+    abc = dirich.sample((HT,)) * 2.0                                    # [HT, 3]
     half = D // 2
     om = torch.rand((half, 2), generator=g) * 0.5 * (16.0 / max(w.height, w.width))
     ph0 = torch.rand((half,), generator=g) * 2 * math.pi
     psi = torch.randn((w.frames, D), generator=g)                        # [F, D]
-    gh = torch.randn((H, D), generator=g)                                # [H, D]
+    gh = torch.randn((HT, D), generator=g)                               # [HT, D]
     n = w.num_blocks
-    sink_mask = torch.zeros((H, n), dtype=torch.bool)
+    sink_mask = torch.zeros((HT, n), dtype=torch.bool)
     sink_mask[:, 0] = True
-    for h in range(H):
+    for h in range(HT):
         idx = torch.randint(0, n, (n_random_sinks,), generator=g)
         sink_mask[h, idx] = True
     # spatial features for the video tokens, [HW, D]
@@ -113,10 +118,11 @@ def family_s(w: Workload, seed: int = SEED_BASE, device="cpu", sigma: float = 0.
     psi_t[w.prefix_tokens:] = psi.repeat_interleave(HW, dim=0)
     tok_block = torch.arange(N) // w.block
     phi_t, psi_t = phi_t.to(dev), psi_t.to(dev)
-    gen_dev = _gen(seed + 1, dev)
     q = torch.empty((B, H, N, D), dtype=torch.bfloat16, device=dev)
     k = torch.empty_like(q)
-    for h in range(H):
+    for hl in range(H):
+        h = head_offset + hl
+        gen_dev = _gen(seed + 1 + 1000 * step + 7919 * h, dev)
         a, b, c = (float(x) for x in abc[h])
         ghh = gh[h].to(dev)
         sinks_tok = sink_mask[h][tok_block].to(dev).float().unsqueeze(1)          # [N, 1]
@@ -128,10 +134,12 @@ def family_s(w: Workload, seed: int = SEED_BASE, device="cpu", sigma: float = 0.
             if w.prefix_tokens:
                 qh[: w.prefix_tokens] = torch.randn((w.prefix_tokens, D), generator=gen_dev, device=dev)
                 kh[: w.prefix_tokens] = torch.randn((w.prefix_tokens, D), generator=gen_dev, device=dev)
-            q[bb, h] = (qh / qh.std()).to(torch.bfloat16)
-            k[bb, h] = (kh / kh.std()).to(torch.bfloat16)
-    gv = _gen(seed + 2, dev)
-    v = torch.randn((B, H, N, D), generator=gv, device=dev, dtype=torch.float32).to(torch.bfloat16)
+            q[bb, hl] = (qh / qh.std()).to(torch.bfloat16)
+            k[bb, hl] = (kh / kh.std()).to(torch.bfloat16)
+    v = torch.empty_like(q)
+    for hl in range(H):
+        gv = _gen(seed + 2 + 7919 * (head_offset + hl), dev)
+        v[:, hl] = torch.randn((B, N, D), generator=gv, device=dev, dtype=torch.float32).to(torch.bfloat16)
     return q, k, v
 
 
