@@ -1,0 +1,32 @@
+"""K4 micro-timing at the Hunyuan shape with structured masks (bring-up experiments).
+MOD_ATTN_DEBUG=1: softmax skipped (MMA+TMA only); =2: K/V TMA skipped; =3 both."""
+import os, sys, json, subprocess
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import synthetic as syn, oracle as O
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
+from gpu_helpers import masks_to_csr, olayout
+import paper_2601_11641_b200 as M
+from bench import attn_flops
+
+w = syn.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "hunyuanvideo-720p"]
+L = olayout(w)
+P = M.Plan(w)
+q, k, v = syn.family_r(w, device="cuda")
+rng = np.random.default_rng(0)
+masks = np.zeros((1, w.heads, L.n, L.n), dtype=bool)
+for h in range(w.heads):
+    sel = O.select_patterns(rng.standard_normal(3 * L.n - 1), L.n, O.SELECT_TOPK, max(4, L.n // 12))
+    masks[0, h] = O.block_mask(sel, rng.random(L.frames) < 0.7, L, True)
+rp, ci = masks_to_csr(masks)
+fl = attn_flops(rp.cpu().numpy(), ci.cpu().numpy(), L.N, L.block, L.head_dim)
+o, lse = P.block_sparse_attn_fwd(q, k, v, rp, ci)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(5):
+    P.block_sparse_attn_fwd(q, k, v, rp, ci, out=o, lse=lse)
+e1.record(); torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / 5
+print(json.dumps({"dbg": os.environ.get("MOD_ATTN_DEBUG", "0"), "density": float(masks.mean()), "ms": ms,
+                  "tflops": fl / ms / 1e9}))
