@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmoddit.so")
+LIB_PATH = os.environ.get("MODDIT_LIB_OVERRIDE") or os.path.join(_HERE, "libmoddit.so")   # override: A/B experiments only
 
 MOD_OK, MOD_ERR_USAGE, MOD_ERR_INPUT, MOD_ERR_NUMERICAL, MOD_ERR_CUDA, MOD_ERR_UNSUPPORTED = range(6)
 STATUS_NAMES = {0: "MOD_OK", 1: "MOD_ERR_USAGE", 2: "MOD_ERR_INPUT", 3: "MOD_ERR_NUMERICAL", 4: "MOD_ERR_CUDA",

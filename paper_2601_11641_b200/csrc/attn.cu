@@ -8,18 +8,21 @@
 // that skipped blocks cost nothing (§5.4 P:460 "block-wise ... block size of 128").
 //
 // Design (one CTA per (b, h, query block); 320 threads, warp-specialised):
-//   warp 0      TMA producer: Q tile once, then K_j / V_j tiles gathered BY INDEX from the CSR
-//               list into a 2-stage shared-memory ring (128B-swizzled boxes, 3D tensor maps so
-//               keys >= N are zero-filled per head).
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer:
-//                  S_j = Q K_j^T       (SS: A = Q smem K-major, B = K_j smem K-major) -> TMEM S[j%2]
-//                  O  += P_j V_j       (TS: A = P_j bf16 in TMEM over S[j%2], B = V_j smem MN-major)
-//               issue order S_0, S_1, PV_0, S_2, PV_1, ... so S_{j+1} and PV_{j-1} overlap softmax j.
-//   warps 2..9  softmax: two threads per query row (column halves); tcgen05.ld of the S row, online softmax in the
-//               log2 domain (ex2.approx), bf16 P written back into TMEM (tcgen05.st), lazy O
-//               rescale only when the running max grows by > 8 (exact: O and l share the
-//               reference max), epilogue O / l -> bf16 and lse.
-// TMEM: S[0] cols [0,BN), S[1] [BN,2BN), O [2BN,2BN+D), l [2BN+D, +16); 512 (or 256) columns.
+//   warp 0      TMA producer: Q once, then K_j / V_j tiles gathered BY INDEX from the CSR list into
+//               shared-memory rings (128B-swizzled boxes; 3D tensor maps zero-fill keys >= N per head).
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer, in the order
+//                  S_0, S_1, PV_0, S_2, PV_1, S_3, ...   (one wait point per PV/S pair)
+//               S_j = Q K_j^T  (SS, fp32 into TMEM S[j%2]);  O_{j%2} += P_j V_j (TS: A = bf16 P_j in TMEM).
+//   warps 2..9  softmax in two independent groups of 4 warps: group g owns the KV blocks j = g mod 2
+//               (split-KV inside the CTA) with its own S buffer, running max / sum and accumulator
+//               O_g.  Each SM sub-partition therefore runs two unsynchronised softmax warps, so the
+//               MUFU pipe (16 ex2/clk/SM -- exactly the tcgen05 rate of a 128x128 tile) stays busy
+//               while the other group reads S or waits; 3/8 of the exponentials run as a
+//               polynomial on the FMA pipe.  Thread = query row: tcgen05.ld of the S row, online
+//               softmax in the log2 domain, bf16 P back into TMEM (tcgen05.st), lazy O rescale only
+//               when the running max grows by > 8 (exact: O_g and l_g share the reference max).
+//               Epilogue: split-KV merge of (m_g, l_g, O_g), O / l -> bf16, lse.
+// TMEM: S[0] [0,BN), S[1] [BN,2BN), O_0 [2BN,2BN+D), O_1 [2BN+D,2BN+2D): 512 (or 256) columns.
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
@@ -31,11 +34,23 @@ using namespace sm100;
 
 namespace {
 
+constexpr int kEmuPairsPer8 = 2;
+// bring-up tracing (MOD_ATTN_DEBUG bit 16): clock64 stamps of one CTA's pipeline events
+constexpr int kTraceCap = 4096;               // events per role
+__device__ long long g_trace[5][kTraceCap][2];  // role: 0 producer, 1 S issuer, 2/3 softmax g0/g1, 4 PV issuer
+__device__ __forceinline__ void trace(int dbg, int role, int& cnt, int tag, int j) {
+  if ((dbg & 16) && blockIdx.x == 1000 && cnt < kTraceCap) {
+    g_trace[role][cnt][0] = clock64();
+    g_trace[role][cnt][1] = ((long long)tag << 32) | (unsigned)j;
+    ++cnt;
+  }
+}
+
 template <int D, int BN>
 struct AttnCfg {
   static constexpr int BM = 128;                      // query rows per tile (tcgen05 M)
-  static constexpr int STAGES = 3;                    // K ring
-  static constexpr int VSTAGES = 2;                   // V ring
+  static constexpr int STAGES = 2;                    // K ring slot = j % 2 = S buffer (k_empty == s_full)
+  static constexpr int VSTAGES = 2;                   // V ring slot = j % 2 = O_g (v_empty == o_done[g])
   static constexpr int Q_BOX = BM * 128;              // bytes of one 64-column box of Q
   static constexpr int KV_BOX = BN * 128;             // bytes of one 64-column box of K or V
   static constexpr int NATOM = D / 64;                // 128B swizzle atoms along D
@@ -44,18 +59,14 @@ struct AttnCfg {
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + Q_BYTES;
   static constexpr int OFF_V = OFF_K + STAGES * KV_BYTES;
-  static constexpr int OFF_ONES = OFF_V + VSTAGES * KV_BYTES;       // all-ones B operand (16 x BN bf16)
-  static constexpr int ONES_BYTES = 16 * BN * 2;
-  static constexpr int OFF_BAR = OFF_ONES + ONES_BYTES;
-  static constexpr int NUM_BARS = 1 + 2 * STAGES + 2 * VSTAGES + 2 + 2 + 1;
-  static constexpr int OFF_RED = OFF_BAR + NUM_BARS * 8 + 16;      // softmax max exchange [2][2][128] f32
+  static constexpr int OFF_BAR = OFF_V + VSTAGES * KV_BYTES;
+  static constexpr int NUM_BARS = 1 + STAGES + VSTAGES + 2 + 2 + 2;
+  static constexpr int OFF_RED = OFF_BAR + NUM_BARS * 8 + 16;      // epilogue (m, l) exchange [2][2][128] f32
   static constexpr int SMEM = OFF_RED + 2 * 2 * 128 * 4;
-  // TMEM columns: S[0] | S[1] | O | l (row sums of the bf16 P, accumulated by the tensor core)
-  static constexpr int TMEM_S0 = 0, TMEM_S1 = BN, TMEM_O = 2 * BN, TMEM_L = 2 * BN + D;
-  static constexpr uint32_t TMEM_COLS = (2 * BN + D + 16) <= 256 ? 256 : 512;
+  static constexpr int TMEM_S0 = 0, TMEM_S1 = BN, TMEM_O = 2 * BN;   // O_g at TMEM_O + g*D
+  static constexpr uint32_t TMEM_COLS = (2 * BN + 2 * D) <= 256 ? 256 : 512;
   static constexpr uint32_t IDESC_S = idesc_bf16_f32(BM, BN, false, false);
   static constexpr uint32_t IDESC_O = idesc_bf16_f32(BM, D, false, true);
-  static constexpr uint32_t IDESC_L = idesc_bf16_f32(BM, 16, false, false);
   static constexpr int THREADS = 320;
 };
 
@@ -66,18 +77,15 @@ __global__ void __launch_bounds__(320, 1)
                     const int* __restrict__ col_idx, __nv_bfloat16* __restrict__ out, float* __restrict__ lse,
                     int N, int n, int block, float scale_log2, int dbg) {
   using C = AttnCfg<D, BN>;
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem = smem_raw;   // 1024-aligned (no static shared memory; checked below)
+  extern __shared__ __align__(1024) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* q_full = bars;
   uint64_t* k_full = bars + 1;
-  uint64_t* k_empty = k_full + C::STAGES;
-  uint64_t* v_full = k_empty + C::STAGES;
-  uint64_t* v_empty = v_full + C::VSTAGES;
-  uint64_t* s_full = v_empty + C::VSTAGES;
+  uint64_t* v_full = k_full + C::STAGES;
+  uint64_t* s_full = v_full + C::VSTAGES;
   uint64_t* p_full = s_full + 2;
   uint64_t* o_done = p_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 1);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0 && (smem_u32(smem) & 1023u) != 0) __trap();   // SWIZZLE_128B needs 1024B alignment
@@ -89,25 +97,14 @@ __global__ void __launch_bounds__(320, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
-    for (int s = 0; s < C::STAGES; ++s) {
-      mbar_init(&k_full[s], 1);
-      mbar_init(&k_empty[s], 1);
-    }
-    for (int s = 0; s < C::VSTAGES; ++s) {
-      mbar_init(&v_full[s], 1);
-      mbar_init(&v_empty[s], 1);
-    }
+    for (int s = 0; s < C::STAGES; ++s) mbar_init(&k_full[s], 1);
+    for (int s = 0; s < C::VSTAGES; ++s) mbar_init(&v_full[s], 1);
     for (int b = 0; b < 2; ++b) {
       mbar_init(&s_full[b], 1);
-      mbar_init(&p_full[b], 256);
+      mbar_init(&p_full[b], 128);
+      mbar_init(&o_done[b], 1);
     }
-    mbar_init(o_done, 1);
     fence_mbar_init();
-  }
-  {  // constant all-ones B operand for the row-sum MMA (swizzle-invariant: every element is 1.0)
-    uint32_t* ones = reinterpret_cast<uint32_t*>(smem + C::OFF_ONES);
-    for (int e = threadIdx.x; e < C::ONES_BYTES / 4; e += blockDim.x) ones[e] = 0x3F803F80u;
-    fence_async_shared();
   }
   if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_slot);
   tc_fence_before();
@@ -122,25 +119,28 @@ __global__ void __launch_bounds__(320, 1)
       tma_prefetch_desc(&tm_k);
       tma_prefetch_desc(&tm_v);
       const uint64_t pol_q = policy_evict_first(), pol_kv = policy_evict_last();
-      unsigned char* sq = smem + C::OFF_Q;
       mbar_arrive_expect_tx(q_full, C::Q_BYTES);
 #pragma unroll
-      for (int a = 0; a < C::NATOM; ++a) tma_load_3d(sq + a * C::Q_BOX, &tm_q, q_full, a * 64, qi * block, bh, pol_q);
+      for (int a = 0; a < C::NATOM; ++a)
+        tma_load_3d(smem + C::OFF_Q + a * C::Q_BOX, &tm_q, q_full, a * 64, qi * block, bh, pol_q);
+      int tc_ = 0;
       auto load_k = [&](int j) {
-        const int s = j % C::STAGES;
-        mbar_wait(&k_empty[s], ((j / C::STAGES) & 1) ^ 1);
+        const int s = j & 1;
+        if (j >= 2) mbar_wait(&s_full[s], ((j - 2) >> 1) & 1);   // S_{j-2} consumed K slot s
+        trace(dbg, 0, tc_, 1, j);
+        if (dbg & 2) { mbar_arrive(&k_full[s]); return; }
         unsigned char* dst = smem + C::OFF_K + s * C::KV_BYTES;
-        if (dbg == 2) { mbar_arrive(&k_full[s]); return; }
         mbar_arrive_expect_tx(&k_full[s], C::KV_BYTES);
         const int row = cols[j] * block;
 #pragma unroll
         for (int a = 0; a < C::NATOM; ++a) tma_load_3d(dst + a * C::KV_BOX, &tm_k, &k_full[s], a * 64, row, bh, pol_kv);
       };
       auto load_v = [&](int j) {
-        const int s = j % C::VSTAGES;
-        mbar_wait(&v_empty[s], ((j / C::VSTAGES) & 1) ^ 1);
+        const int s = j & 1;
+        if (j >= 2) mbar_wait(&o_done[s], ((j - 2) >> 1) & 1);   // PV_{j-2} consumed V slot s
+        trace(dbg, 0, tc_, 2, j);
+        if (dbg & 2) { mbar_arrive(&v_full[s]); return; }
         unsigned char* dst = smem + C::OFF_V + s * C::KV_BYTES;
-        if (dbg == 2) { mbar_arrive(&v_full[s]); return; }
         mbar_arrive_expect_tx(&v_full[s], C::KV_BYTES);
         const int row = cols[j] * block;
 #pragma unroll
@@ -155,166 +155,189 @@ __global__ void __launch_bounds__(320, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
+    // tcgen05.mma issue blocks while the pipe is busy (shallow queue): every wait of this thread
+    // drains the pipe, so the loop has few wait points and one commit per MMA group:
+    //   S_0, S_1, then per j:  [wait V_j, P_j] PV_j -> O_{j%2}   [wait K_{j+2}] S_{j+2} -> S[j%2]
     if (lane == 0 && L > 0) {
       const uint32_t sq = smem_u32(smem + C::OFF_Q);
       mbar_wait(q_full, 0);
       tc_fence_after();
-      for (int j = 0; j <= L; ++j) {
-        if (j < L) {
-          const int s = j % C::STAGES;
-          mbar_wait(&k_full[s], (j / C::STAGES) & 1);
-          tc_fence_after();
-          const uint32_t sk = smem_u32(smem + C::OFF_K + s * C::KV_BYTES);
-          const uint32_t d_s = tmem + ((j & 1) ? C::TMEM_S1 : C::TMEM_S0);
+      int tc_ = 0;
+      auto issue_s = [&](int j) {
+        const int b = j & 1;
+        mbar_wait(&k_full[b], (j >> 1) & 1);
+        trace(dbg, 1, tc_, 10, j);
+        tc_fence_after();
+        const uint32_t sk = smem_u32(smem + C::OFF_K + b * C::KV_BYTES);
+        const uint32_t d_s = tmem + (b ? C::TMEM_S1 : C::TMEM_S0);
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t off = (kk / 4) * 0 + (kk % 4) * 32;
-            const uint64_t ad = smem_desc_sw128(sq + (kk / 4) * C::Q_BOX + off, 16, 1024);
-            const uint64_t bd = smem_desc_sw128(sk + (kk / 4) * C::KV_BOX + off, 16, 1024);
-            mma_ss(d_s, ad, bd, C::IDESC_S, kk > 0 ? 1u : 0u);
-          }
-          mma_commit(&k_empty[s]);
-          mma_commit(&s_full[j & 1]);
+        for (int kk = 0; kk < D / 16; ++kk) {
+          // K-major SW128: 32 bytes per K step inside a 128B atom, atoms one box apart
+          const uint64_t ad = smem_desc_sw128(sq + (kk / 4) * C::Q_BOX + (kk % 4) * 32, 16, 1024);
+          const uint64_t bd = smem_desc_sw128(sk + (kk / 4) * C::KV_BOX + (kk % 4) * 32, 16, 1024);
+          mma_ss(d_s, ad, bd, C::IDESC_S, kk > 0 ? 1u : 0u);
         }
-        if (j >= 1) {
-          const int jj = j - 1;
-          const int s = jj % C::VSTAGES;
-          mbar_wait(&p_full[jj & 1], (jj >> 1) & 1);
-          mbar_wait(&v_full[s], (jj / C::VSTAGES) & 1);
-          tc_fence_after();
-          const uint32_t sv = smem_u32(smem + C::OFF_V + s * C::KV_BYTES);
-          const uint32_t p_t = tmem + ((jj & 1) ? C::TMEM_S1 : C::TMEM_S0);
+        mma_commit(&s_full[b]);          // also releases K slot b to the producer
+        trace(dbg, 1, tc_, 11, j);
+      };
+      issue_s(0);
+      if (L > 1) issue_s(1);
+      for (int j = 0; j < L; ++j) {
+        const int b = j & 1;
+        mbar_wait(&v_full[b], (j >> 1) & 1);
+        mbar_wait(&p_full[b], (j >> 1) & 1);
+        trace(dbg, 1, tc_, 12, j);
+        tc_fence_after();
+        const uint32_t sv = smem_u32(smem + C::OFF_V + b * C::KV_BYTES);
+        const uint32_t p_t = tmem + (b ? C::TMEM_S1 : C::TMEM_S0);
 #pragma unroll
-          const uint32_t s_ones = smem_u32(smem + C::OFF_ONES);
-#pragma unroll
-          for (int kk = 0; kk < BN / 16; ++kk) {
-            // B = V_j: N = D (MN-major, 64-column atoms LBO = KV_BOX apart), K = 16 keys = 2048 bytes
-            const uint64_t bd = smem_desc_sw128(sv + kk * 2048, C::KV_BOX, 1024);
-            mma_ts(tmem + C::TMEM_O, p_t + kk * 8, bd, C::IDESC_O, (jj > 0 || kk > 0) ? 1u : 0u);
-            // l += P_j 1  (N = 16 all-ones columns, K-major)
-            const uint64_t ld = smem_desc_sw128(s_ones + (kk / 4) * 2048 + (kk % 4) * 32, 16, 1024);
-            mma_ts(tmem + C::TMEM_L, p_t + kk * 8, ld, C::IDESC_L, (jj > 0 || kk > 0) ? 1u : 0u);
-          }
-          mma_commit(&v_empty[s]);
-          mma_commit(o_done);
+        for (int kk = 0; kk < BN / 16; ++kk) {
+          // B = V_j: N = D (MN-major, 64-column atoms LBO = KV_BOX apart), K = 16 keys = 2048 bytes
+          const uint64_t bd = smem_desc_sw128(sv + kk * 2048, C::KV_BOX, 1024);
+          mma_ts(tmem + C::TMEM_O + b * D, p_t + kk * 8, bd, C::IDESC_O, (j > 1 || kk > 0) ? 1u : 0u);
         }
+        mma_commit(&o_done[b]);          // also releases V slot b to the producer
+        trace(dbg, 1, tc_, 14, j);
+        if (j + 2 < L) issue_s(j + 2);   // S[b] is free once PV_j (issued above, in order) read P_j
       }
     }
-  } else if (warp >= 2) {
-    // ------------------------------------------------------------ softmax / epilogue (8 warps)
-    // Two threads per query row: warps w and w+4 read the same TMEM lane quarter and split the BN
-    // score columns (and, in the epilogue, the D output columns) in halves, so every SM
-    // sub-partition runs two independent softmax warps (latency hiding).  Per element: one FFMA
-    // (s*log2e/sqrt(d) - m) and half a MUFU: pairs are packed to bf16x2 and exponentiated with
-    // ex2.approx.bf16x2, which yields P in the packed format the PV MMA consumes.  The row sum l is
-    // not accumulated here: the tensor core computes l += P*1 next to O += P*V, so O and l see
-    // exactly the same rounded P.
-    constexpr int CPT = BN / 2;                // score columns per thread
-    constexpr int OPT = D / 2;                 // output columns per thread (epilogue)
-    auto red_max = reinterpret_cast<float(*)[2][128]>(smem + C::OFF_RED);   // [iter parity][half][row]
-    const int half = (warp - 2) >> 2;
-    const int quarter = warp & 3;              // TMEM lane quarter this warp may access
-    const int row = quarter * 32 + lane;       // query row within the tile
+  } else {
+    // ------------------------------------------------------------ softmax / epilogue (2 groups x 4 warps)
+    const int g = (warp - 2) >> 2;
+    const int quarter = warp & 3;          // TMEM lane quarter this warp may access
+    const int row = quarter * 32 + lane;   // query row within the tile
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const uint32_t t_s = tmem + lane_off + (g ? C::TMEM_S1 : C::TMEM_S0);
+    const uint32_t t_og = tmem + lane_off + C::TMEM_O + g * D;
     const int q_row0 = qi * block;
     const int q_rows = min(block, N - q_row0);
-    float m_run = -INFINITY;
-    for (int j = 0; j < L; ++j) {
-      const int b = j & 1;
-      const uint32_t t_s = tmem + lane_off + (b ? C::TMEM_S1 : C::TMEM_S0);
-      mbar_wait(&s_full[b], (j >> 1) & 1);
+    float m_run = -INFINITY, l_run = 0.f;
+    int it = 0, tc_ = 0;
+    for (int j = g; j < L; j += 2, ++it) {
+      mbar_wait(&s_full[g], it & 1);
+      if (lane == 0 && quarter == 2) trace(dbg, 2 + g, tc_, 20 + g, j);
       tc_fence_after();
-      uint32_t sr[CPT];
+      if (dbg & 1) {   // bring-up: MMA/TMA pipeline without the softmax math
+        if (it >= 1) mbar_wait(&o_done[g], (it - 1) & 1);
+        tc_fence_before();
+        mbar_arrive(&p_full[g]);
+        continue;
+      }
+      uint32_t sr[BN];
 #pragma unroll
-      for (int c = 0; c < CPT / 32; ++c)
-        tmem_ld32(t_s + half * CPT + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
+      for (int c = 0; c < BN / 32; ++c) tmem_ld32(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
       tmem_ld_wait();
       float* s = reinterpret_cast<float*>(sr);
-      const int kv_valid = N - cols[j] * block - half * CPT;  // valid keys among this thread's columns
-      if (kv_valid < CPT) {
+      const int kv_valid = N - cols[j] * block;  // keys of this block inside the sequence
+      if (kv_valid < BN) {
 #pragma unroll
-        for (int c = 0; c < CPT; ++c)
+        for (int c = 0; c < BN; ++c)
           if (c >= kv_valid) s[c] = -INFINITY;
       }
       float mxv[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) mxv[u] = s[u];
 #pragma unroll
-      for (int c = 8; c < CPT; c += 8)
+      for (int c = 8; c < BN; c += 8)
 #pragma unroll
         for (int u = 0; u < 8; ++u) mxv[u] = fmaxf(mxv[u], s[c + u]);
-      float mx = fmaxf(fmaxf(fmaxf(mxv[0], mxv[1]), fmaxf(mxv[2], mxv[3])),
-                       fmaxf(fmaxf(mxv[4], mxv[5]), fmaxf(mxv[6], mxv[7])));
-      red_max[b][half][row] = mx;
-      named_bar_sync(1 + quarter, 64);
-      mx = fmaxf(mx, red_max[b][half ^ 1][row]);
+      const float mx = fmaxf(fmaxf(fmaxf(mxv[0], mxv[1]), fmaxf(mxv[2], mxv[3])),
+                             fmaxf(fmaxf(mxv[4], mxv[5]), fmaxf(mxv[6], mxv[7])));
       const float m_new = fmaxf(m_run, mx * scale_log2);
       const bool rescale = (m_new - m_run) > 8.0f;   // also true on the first block (m_run = -inf)
       const float m_use = rescale ? m_new : m_run;
       const float alpha = rescale ? ex2(m_run - m_new) : 1.0f;
-      m_run = m_use;
-      uint32_t pk[CPT / 2];
+      // packed fp32x2 FMA-pipe ops (FFMA2 / FADD2): x = s*log2e/sqrt(d) - m per pair; a share of the
+      // pairs is exponentiated by a polynomial on the FMA pipe, the rest by MUFU ex2 (16/clk/SM, the
+      // tcgen05 rate of a 128x128 tile, so MUFU alone would pace the whole loop)
+      const float2 sc2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-m_use, -m_use);
+      float2 acc2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      uint32_t pk[BN / 2];
 #pragma unroll
-      for (int c = 0; c < CPT; c += 2)
-        pk[c / 2] = ex2_bf16x2(pack_bf16(fmaf(s[c], scale_log2, -m_use), fmaf(s[c + 1], scale_log2, -m_use)));
-      if constexpr (CPT / 2 == 32) tmem_st32(t_s + half * (CPT / 2), *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
-      else tmem_st16(t_s + half * (CPT / 2), *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
-      if (j >= 1) {
-        mbar_wait(o_done, (j - 1) & 1);   // PV_{j-1} finished writing O and l
+      for (int c = 0; c < BN; c += 2) {
+        const float2 x = ffma2(make_float2(s[c], s[c + 1]), sc2, nm2);
+        float2 p;
+        if (((c / 2) & 7) < kEmuPairsPer8) {
+          p = ex2_poly2(x);
+        } else {
+          p.x = ex2(x.x);
+          p.y = ex2(x.y);
+        }
+        acc2[(c / 2) & 1] = fadd2(acc2[(c / 2) & 1], p);
+        pk[c / 2] = pack_bf16(p.x, p.y);
+      }
+      l_run = fmaf(l_run, alpha, (acc2[0].x + acc2[0].y) + (acc2[1].x + acc2[1].y));
+      m_run = m_use;
+      if (lane == 0 && quarter == 2) trace(dbg, 2 + g, tc_, 30 + g, j);
+#pragma unroll
+      for (int c = 0; c < BN / 64; ++c) tmem_st32(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[c * 32]));
+      if (it >= 1) {
+        mbar_wait(&o_done[g], (it - 1) & 1);   // this group's previous PV finished writing O_g
         tc_fence_after();
         if (__any_sync(0xffffffffu, rescale)) {
-          const uint32_t t_o = tmem + lane_off + C::TMEM_O + half * OPT;
 #pragma unroll
-          for (int c = 0; c < OPT / 32; ++c) {
+          for (int c = 0; c < D / 32; ++c) {
             uint32_t o[32];
-            tmem_ld32(t_o + c * 32, o);
+            tmem_ld32(t_og + c * 32, o);
             tmem_ld_wait();
 #pragma unroll
             for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-            tmem_st32(t_o + c * 32, o);
-          }
-          if (half == 0) {
-            uint32_t lv = tmem_ld1(tmem + lane_off + C::TMEM_L);
-            tmem_ld_wait();
-            tmem_st1(tmem + lane_off + C::TMEM_L, __float_as_uint(__uint_as_float(lv) * alpha));
+            tmem_st32(t_og + c * 32, o);
           }
         }
       }
       tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(&p_full[b]);
+      mbar_arrive(&p_full[g]);
+      if (lane == 0 && quarter == 2) trace(dbg, 2 + g, tc_, 40 + g, j);
     }
-    // epilogue: O / l -> bf16 (each thread of the pair writes half of the row), lse
+    // epilogue: merge the two split-KV partial results, O / l -> bf16, lse
+    auto red = reinterpret_cast<float(*)[2][128]>(smem + C::OFF_RED);   // [group][m|l][row]
+    red[g][0][row] = m_run;
+    red[g][1][row] = l_run;
+    named_bar_sync(1, 256);
+    const int n0 = (L + 1) / 2, n1 = L / 2;   // blocks handled by group 0 / 1
+    const float m0 = red[0][0][row], l0 = red[0][1][row], m1 = red[1][0][row], l1 = red[1][1][row];
     const bool valid = row < q_rows;
     const size_t grow = (size_t)bh * N + q_row0 + row;
     if (L > 0) {
-      mbar_wait(o_done, (L - 1) & 1);
+      mbar_wait(&o_done[0], (n0 - 1) & 1);
+      if (n1 > 0) mbar_wait(&o_done[1], (n1 - 1) & 1);
       tc_fence_after();
-      const float l = __uint_as_float(tmem_ld1(tmem + lane_off + C::TMEM_L));
-      tmem_ld_wait();
-      const float inv_l = 1.0f / l;
-      const uint32_t t_o = tmem + lane_off + C::TMEM_O + half * OPT;
+      const float m = fmaxf(m0, m1);
+      const float f0 = ex2(m0 - m);
+      const float f1 = n1 > 0 ? ex2(m1 - m) : 0.f;
+      const float l = l0 * f0 + l1 * f1;
+      const float a0 = f0 / l, a1 = f1 / l;
+      const uint32_t t_o0 = tmem + lane_off + C::TMEM_O + g * (D / 2);
 #pragma unroll
-      for (int c = 0; c < OPT / 32; ++c) {
-        uint32_t o[32];
-        tmem_ld32(t_o + c * 32, o);
+      for (int c = 0; c < D / 64; ++c) {
+        uint32_t o0[32], o1[32];
+        tmem_ld32(t_o0 + c * 32, o0);
+        if (n1 > 0) tmem_ld32(t_o0 + D + c * 32, o1);
         tmem_ld_wait();
         uint32_t pkd[16];
 #pragma unroll
-        for (int e = 0; e < 16; ++e)
-          pkd[e] = pack_bf16(__uint_as_float(o[2 * e]) * inv_l, __uint_as_float(o[2 * e + 1]) * inv_l);
+        for (int e = 0; e < 16; ++e) {
+          float x0 = __uint_as_float(o0[2 * e]) * a0, x1 = __uint_as_float(o0[2 * e + 1]) * a0;
+          if (n1 > 0) {
+            x0 = fmaf(__uint_as_float(o1[2 * e]), a1, x0);
+            x1 = fmaf(__uint_as_float(o1[2 * e + 1]), a1, x1);
+          }
+          pkd[e] = pack_bf16(x0, x1);
+        }
         if (valid) {
-          int4* dst = reinterpret_cast<int4*>(out + grow * D + half * OPT + c * 32);
+          int4* dst = reinterpret_cast<int4*>(out + grow * D + g * (D / 2) + c * 32);
 #pragma unroll
           for (int e = 0; e < 4; ++e) dst[e] = make_int4(pkd[4 * e], pkd[4 * e + 1], pkd[4 * e + 2], pkd[4 * e + 3]);
         }
       }
-      if (valid && lse && half == 0) lse[grow] = (m_run + __log2f(l)) * 0.69314718055994531f;
+      if (valid && lse && g == 0) lse[grow] = (m + __log2f(l)) * 0.69314718055994531f;
     } else if (valid) {
-      int4* dst = reinterpret_cast<int4*>(out + grow * D + half * OPT);
+      int4* dst = reinterpret_cast<int4*>(out + grow * D + g * (D / 2));
 #pragma unroll
-      for (int e = 0; e < OPT / 8; ++e) dst[e] = make_int4(0, 0, 0, 0);
-      if (lse && half == 0) lse[grow] = -INFINITY;
+      for (int e = 0; e < D / 16; ++e) dst[e] = make_int4(0, 0, 0, 0);
+      if (lse && g == 0) lse[grow] = -INFINITY;
     }
   }
   tc_fence_before();
@@ -374,6 +397,17 @@ mod_status launch(mod_plan P, const void* q, const void* k, const void* v, const
 }
 
 }  // namespace
+
+// bring-up only (not in moddit.h): copies the trace of the last MOD_ATTN_DEBUG&16 launch
+extern "C" int mod_debug_attn_trace(long long* host, int cap) {
+  // host receives [4][kTraceCap][2]; unused slots are zero
+  if (cap < 5 * kTraceCap * 2) return -1;
+  cudaMemcpyFromSymbol(host, g_trace, sizeof(long long) * 5 * kTraceCap * 2);
+  cudaMemset(nullptr, 0, 0);
+  static long long zeros[5 * kTraceCap * 2];
+  cudaMemcpyToSymbol(g_trace, zeros, sizeof(zeros));
+  return 5 * kTraceCap;
+}
 
 extern "C" mod_status mod_block_sparse_attn_fwd(mod_plan P, const void* q, const void* k, const void* v,
                                                 const int32_t* row_ptr, const int32_t* col_idx, void* o, float* lse,

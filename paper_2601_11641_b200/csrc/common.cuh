@@ -8,7 +8,7 @@
 #include <string>
 #include <vector>
 
-#include "../../include/moddit.h"
+#include "moddit.h"
 
 // ------------------------------------------------------------------------------------------------
 // error handling (thread-local message, see mod_last_error)

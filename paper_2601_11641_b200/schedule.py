@@ -1,0 +1,85 @@
+"""Algorithm 1 of MOD-DiT for one attention layer, driving the C-ABI kernels.
+
+    t = 1..m           full attention (all-ones index lists; FlashAttention-2 in the paper)
+    t = m-1, m         pooled statistics + mixture fit  X^(m-1), X^(m)
+    t = m              block-diagonal keep decision; history seeded with W^(m)
+    t > m              mask = predict(x_prev, x_curr; t) (Eq. 6/7 + §5.3) -> block-sparse attention
+    t = t_p^(i) = m + i*dt (i >= 1)   after the attention: fresh statistics, Eq. 5 merge, refit, roll
+                                      (reading Z9: t_p^(i) = m + i*dt, not "t mod dt == 0"; Z11: the
+                                      attention at t_p uses the previous window's prediction)
+All state is plain device tensors (checkpointable with torch.save); everything is stream-ordered and
+no host synchronisation happens inside ``step``.
+"""
+from __future__ import annotations
+
+import dataclasses
+
+import torch
+
+from .plan import Plan
+
+
+@dataclasses.dataclass
+class ScheduleState:
+    t_prev: int = -1
+    t_curr: int = -1
+    x_prev: torch.Tensor | None = None
+    x_curr: torch.Tensor | None = None
+    keep: torch.Tensor | None = None
+    hist: torch.Tensor | None = None
+    W_warm: torch.Tensor | None = None
+
+
+class Schedule:
+    def __init__(self, plan: Plan, T: int = 50, m: int = 12, dt: int = 10, top_k: int | None = None,
+                 select_mode: int | None = None, select_param: float | None = None):
+        if not (1 <= m < T) or dt < 1 or m < 2:
+            raise ValueError(f"bad schedule T={T} m={m} dt={dt}")
+        self.P, self.T, self.m, self.dt = plan, T, m, dt
+        self.sel = dict(top_k=top_k, select_mode=select_mode, select_param=select_param)
+        self.state = ScheduleState()
+        self._dense = None
+        self.last_mask = None
+
+    def is_update_step(self, t: int) -> bool:
+        """t is a prediction step t_p^(i) = m + i*dt with i >= 1."""
+        return t > self.m and (t - self.m) % self.dt == 0
+
+    def dense_mask(self):
+        if self._dense is None:
+            self._dense = self.P.dense_mask()
+        return self._dense
+
+    def step(self, t: int, q, k, v, out=None, lse=None):
+        P, S = self.P, self.state
+        if not 1 <= t <= self.T:
+            raise ValueError(f"t={t} outside [1, {self.T}]")
+        if t <= self.m:
+            rp, ci = self.dense_mask()
+            o, l = P.block_sparse_attn_fwd(q, k, v, rp, ci, out=out, lse=lse)
+            if t == self.m - 1:
+                S.W_warm = P.collect_block_stats(q, k)
+                S.x_prev, S.t_prev = P.fit_mixture(S.W_warm), t
+            elif t == self.m:
+                W = P.collect_block_stats(q, k)
+                S.x_curr, S.t_curr = P.fit_mixture(W), t
+                S.keep = P.keep_frames(S.x_prev, S.x_curr)
+                S.hist = W                                    # A_hat^(t_p^(0)) = A^(m)
+                S.W_warm = None
+            self.last_mask = (rp, ci)
+            return o, l
+        rp, ci = P.predict_block_mask(S.x_prev, S.x_curr, S.t_prev, S.t_curr, t, S.keep, **self.sel)
+        o, l = P.block_sparse_attn_fwd(q, k, v, rp, ci, out=out, lse=lse)
+        if self.is_update_step(t):
+            W = P.collect_block_stats(q, k)
+            P.update_online_mask(W, rp, ci, S.hist, S.x_prev, S.x_curr)
+            S.t_prev, S.t_curr = S.t_curr, t
+        self.last_mask = (rp, ci)
+        return o, l
+
+    def state_dict(self) -> dict:
+        return {f.name: getattr(self.state, f.name) for f in dataclasses.fields(self.state) if f.name != "W_warm"}
+
+    def load_state_dict(self, d: dict):
+        for k, v in d.items():
+            setattr(self.state, k, v)

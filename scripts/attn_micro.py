@@ -22,11 +22,21 @@ rp, ci = masks_to_csr(masks)
 fl = attn_flops(rp.cpu().numpy(), ci.cpu().numpy(), L.N, L.block, L.head_dim)
 o, lse = P.block_sparse_attn_fwd(q, k, v, rp, ci)
 torch.cuda.synchronize()
+import threading, pynvml
+pynvml.nvmlInit(); hnd = pynvml.nvmlDeviceGetHandleByIndex(0); clk = []; stop = threading.Event()
+def samp():
+    while not stop.is_set():
+        clk.append(pynvml.nvmlDeviceGetClockInfo(hnd, pynvml.NVML_CLOCK_SM)); stop.wait(0.01)
+th = threading.Thread(target=samp); th.start()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
-for _ in range(5):
+REPS = int(os.environ.get("REPS", "5"))
+for _ in range(REPS):
     P.block_sparse_attn_fwd(q, k, v, rp, ci, out=o, lse=lse)
-e1.record(); torch.cuda.synchronize()
-ms = e0.elapsed_time(e1) / 5
-print(json.dumps({"dbg": os.environ.get("MOD_ATTN_DEBUG", "0"), "density": float(masks.mean()), "ms": ms,
-                  "tflops": fl / ms / 1e9}))
+e1.record(); torch.cuda.synchronize(); stop.set(); th.join()
+ms = e0.elapsed_time(e1) / REPS
+mhz = float(np.median(clk)) if clk else float("nan")
+nnz = float(masks.sum()); iters_per_sm = nnz / 148
+print(json.dumps({"lib": os.environ.get("MODDIT_LIB_OVERRIDE", "default"), "dbg": os.environ.get("MOD_ATTN_DEBUG", "0"),
+                  "density": round(float(masks.mean()), 4), "ms": round(ms, 3), "tflops": round(fl / ms / 1e9, 1),
+                  "sm_mhz": mhz, "cycles_per_block_iter": round(ms * 1e-3 * mhz * 1e6 / iters_per_sm, 1)}))

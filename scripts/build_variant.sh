@@ -1,0 +1,10 @@
+#!/bin/bash
+# build_variant.sh NAME ATTN_CU : libmoddit.so with an alternative attn.cu into _variants/NAME/ (A/B experiments)
+set -e
+NAME=$1; SRC=$2
+D=$(mktemp -d); cp -r paper_2601_11641_b200/csrc $D/csrc; cp $SRC $D/csrc/attn.cu
+mkdir -p _variants/$NAME
+objs=""
+for f in $D/csrc/*.cu; do o=$D/$(basename $f .cu).o; nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr -I include -I $D/csrc -c $f -o $o & objs="$objs $o"; done; wait
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o _variants/$NAME/libmoddit.so $objs
+rm -rf $D; echo _variants/$NAME/libmoddit.so

@@ -1,0 +1,67 @@
+// tcgen05.mma issue-rate calibration on sm_100a (bring-up microbenchmark, not part of libmoddit):
+// one CTA per SM, one thread issues NITER back-to-back kind::f16 MMAs (bf16 in, fp32 accumulate).
+#include <cstdio>
+#include <cstdint>
+#include "../../paper_2601_11641_b200/csrc/sm100.cuh"
+using namespace sm100;
+template <int N, bool TS>
+__global__ void __launch_bounds__(128, 1) k(long long* cyc, int niter) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ uint32_t slot;
+  __shared__ __align__(8) uint64_t bar;
+  for (int i = threadIdx.x; i < 160 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0;
+  fence_async_shared();
+  if (threadIdx.x < 32) tmem_alloc<512>(&slot);
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_mbar_init(); }
+  tc_fence_before(); __syncthreads(); tc_fence_after();
+  const uint32_t tmem = slot;
+  if (threadIdx.x == 0) {
+    constexpr uint32_t idesc = idesc_bf16_f32(128, N, false, false);
+    const uint32_t sa = smem_u32(smem), sb = smem_u32(smem + 32768);  // B: up to 256 rows x 2 atoms = 64KB
+    long long t0 = clock64();
+    for (int it = 0; it < niter; ++it) {
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const uint64_t bd = smem_desc_sw128(sb + (kk / 4) * (N * 128) + (kk % 4) * 32, 16, 1024);
+        if (TS) mma_ts(tmem, tmem + 384 + kk * 8, bd, idesc, 1u);
+        else {
+          const uint64_t ad = smem_desc_sw128(sa + (kk / 4) * 16384 + (kk % 4) * 32, 16, 1024);
+          mma_ss(tmem, ad, bd, idesc, 1u);
+        }
+      }
+    }
+    mma_commit(&bar);
+    mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    cyc[blockIdx.x] = t1 - t0;
+  }
+  tc_fence_before(); __syncthreads();
+  if (threadIdx.x < 32) { tc_fence_after(); tmem_dealloc<512>(tmem); }
+}
+template <int N, bool TS> void run(const char* name) {
+  long long* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, 148 * 8);
+  printf("malloc %s\n", cudaGetErrorString(e)); fflush(stdout);
+  auto kern = k<N, TS>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024 + 1024);
+  int niter = 2000;
+  kern<<<148, 128, 160 * 1024 + 1024>>>(d, niter);
+  printf("first launch %s\n", cudaGetErrorString(cudaDeviceSynchronize())); fflush(stdout);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  cudaEventRecord(e0); kern<<<148, 128, 160 * 1024 + 1024>>>(d, niter); cudaEventRecord(e1); cudaEventSynchronize(e1);
+  float ms; cudaEventElapsedTime(&ms, e0, e1);
+  long long h[148]; cudaMemcpy(h, d, 148 * 8, cudaMemcpyDeviceToHost);
+  double avg = 0; for (int i = 0; i < 148; ++i) avg += h[i]; avg /= 148;
+  double flops = 148.0 * niter * 8 * 2.0 * 128 * N * 16;
+  printf("%-14s %s cycles/MMA=%.1f  ideal=%d  TFLOPS=%.0f  (%.3f ms) err=%s\n", name, TS ? "TS" : "SS", avg / (niter * 8.0),
+         128 * N / 256, flops / ms / 1e9, ms, cudaGetErrorString(cudaGetLastError()));
+}
+int main() {
+  run<128, false>("M128 N128 K16");
+  run<256, false>("M128 N256 K16");
+  run<64, false>("M128 N64 K16");
+  run<128, true>("M128 N128 K16");
+  run<256, true>("M128 N256 K16");
+  return 0;
+}

@@ -1,0 +1,63 @@
+"""Head partitioning and the Ulysses all-to-all on CPU with gloo, world size 2 and 4."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2601_11641_b200.parallel import head_range, heads_to_seq, lpt_head_assignment, seq_to_heads
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, ws, port, B, N, H, D, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    try:
+        g = torch.Generator().manual_seed(0)
+        full = torch.randn((B, N, H, D), generator=g)         # [B, N, H, D] activations, identical on all ranks
+        Ns = N // ws
+        x_seq = full[:, rank * Ns:(rank + 1) * Ns].contiguous()
+        x_head = seq_to_heads(x_seq)
+        h0, h1 = head_range(H, ws, rank)
+        ref = full.permute(0, 2, 1, 3)[:, h0:h1].contiguous()  # [B, H/P, N, D]
+        ok1 = torch.equal(x_head, ref)
+        back = heads_to_seq(x_head)
+        ok2 = torch.equal(back, x_seq)
+        q.put((rank, ok1, ok2))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("ws", [2, 4])
+def test_ulysses_roundtrip_gloo(ws):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, ws, port, 2, 24, 8, 16, q)) for r in range(ws)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(ws)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(r[1] and r[2] for r in res), res
+
+
+def test_head_range_and_lpt():
+    assert [head_range(24, 8, r) for r in range(8)][-1] == (21, 24)
+    with pytest.raises(ValueError):
+        head_range(24, 5, 0)
+    parts = lpt_head_assignment([5, 1, 4, 2, 3, 3], 2)
+    assert sorted(sum(parts, [])) == list(range(6))
+    loads = [sum([5, 1, 4, 2, 3, 3][h] for h in p) for p in parts]
+    assert max(loads) - min(loads) <= 1
