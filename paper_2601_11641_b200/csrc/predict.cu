@@ -1,6 +1,6 @@
 // predict.cu -- K2b mod_predict_block_mask (+ the dense all-ones mask helper).
 //
-// Per head (one CTA, 1024 threads):
+// Per head:
 //  1. linear prediction (§5.2 Eq. 6, Eq. 7) of the C and D
 //     intensities, evaluated in IEEE fp64 without contraction so that the integer decisions below
 //     match the oracle bit for bit:  d = x_c - x_p;  s = d / (t_c - t_p);  x_hat = x_c + s*(t - t_c);
@@ -9,8 +9,9 @@
 //     compares directly.  TOPMASS accumulates max(key,0)*|supp| sequentially in sorted order;
 //  3. block mask = selected diagonals (j - i = delta_k) | selected columns | kept frame squares
 //     [a_r,b_r]^2 | diagonal guard | prefix rows/columns (Alg. 1; Z15, Z17),
-//     emitted as a CSR index list: a warp per row, ballot + popc for the counts and the write
-//     positions, one block-wide scan for the row pointers.
+//     emitted as a CSR index list.  Steps 1 (one CTA per head), 2 (row counts) and 3 (row
+//     pointers + column lists) are separate launches so that the O(n^2) mask work spreads over
+//     (row chunk, head) CTAs: a warp per row, ballot + popc for counts and write positions.
 #include "common.cuh"
 
 namespace {
@@ -27,6 +28,8 @@ struct PredictArgs {
   const int* row_frames;
   int* row_ptr;
   int* col_idx;
+  uint8_t* sel;    // workspace [BH, 3n-1]: selected C/D patterns
+  int* cnt;        // workspace [BH, n]: passing blocks per row
   int n, F, p, prefix_last, diag_guard, mode, top_k;
   double param;
   double dt_hist;  // t_curr - t_prev
@@ -34,21 +37,18 @@ struct PredictArgs {
   int P2;          // sort size (power of two >= 3n-1)
 };
 
-__global__ void __launch_bounds__(1024) predict_kernel(PredictArgs a) {
+// 1. keys + selection, one CTA per head
+__global__ void __launch_bounds__(1024) select_kernel(PredictArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int n = a.n, P = 3 * n - 1, P2 = a.P2;
   double* keys = reinterpret_cast<double*>(smem);
   int* ids = reinterpret_cast<int*>(keys + P2);
-  int* cnt = ids + P2;                                   // [n + 1]
-  unsigned char* sel = reinterpret_cast<unsigned char*>(cnt + n + 1);   // [P]
-  __shared__ int warp_tot[32];
   __shared__ int sel_len;
   const int t = threadIdx.x;
   const size_t bh = blockIdx.x;
   const double* xp = a.x_prev + bh * a.p;
   const double* xc = a.x_curr + bh * a.p;
-
-  // 1. keys
+  uint8_t* sel = a.sel + bh * P;
   for (int e = t; e < P2; e += blockDim.x) {
     if (e < P) {
       const double c = xc[e];
@@ -60,128 +60,157 @@ __global__ void __launch_bounds__(1024) predict_kernel(PredictArgs a) {
     }
     ids[e] = e;
   }
-  for (int e = t; e < P; e += blockDim.x) sel[e] = 0;
   __syncthreads();
-
-  // 2. selection
   if (a.mode == MOD_SELECT_THRESHOLD) {
     for (int e = t; e < P; e += blockDim.x) sel[e] = keys[e] > a.param;
-  } else {
-    for (int k = 2; k <= P2; k <<= 1) {
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        for (int i = t; i < P2; i += blockDim.x) {
-          const int l = i ^ j;
-          if (l > i) {
-            const double ki = keys[i], kl = keys[l];
-            const int ii = ids[i], il = ids[l];
-            const bool up = (i & k) == 0;
-            const bool sw = up ? before(kl, il, ki, ii) : before(ki, ii, kl, il);
-            if (sw) {
-              keys[i] = kl; keys[l] = ki;
-              ids[i] = il; ids[l] = ii;
-            }
+    return;
+  }
+  for (int k = 2; k <= P2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = t; i < P2; i += blockDim.x) {
+        const int l = i ^ j;
+        if (l > i) {
+          const double ki = keys[i], kl = keys[l];
+          const int ii = ids[i], il = ids[l];
+          const bool up = (i & k) == 0;
+          const bool sw = up ? before(kl, il, ki, ii) : before(ki, ii, kl, il);
+          if (sw) {
+            keys[i] = kl; keys[l] = ki;
+            ids[i] = il; ids[l] = ii;
           }
         }
-        __syncthreads();
       }
+      __syncthreads();
     }
-    if (t == 0) {
-      int L = 0;
-      if (a.mode == MOD_SELECT_TOPK) {
-        L = min(a.top_k, P);
-      } else {  // TOPMASS
-        double acc = 0.0;
+  }
+  if (t == 0) {
+    int L = 0;
+    if (a.mode == MOD_SELECT_TOPK) {
+      L = min(a.top_k, P);
+    } else {  // TOPMASS: sequential fp64 sum in sorted order (bit-identical to the oracle)
+      double acc = 0.0;
+      for (int e = 0; e < P; ++e) {
+        const int id = ids[e];
+        const double supp = id < 2 * n - 1 ? (double)(n - abs(id - (n - 1))) : (double)n;
+        acc = __dadd_rn(acc, __dmul_rn(fmax(keys[e], 0.0), supp));
+      }
+      if (acc > 0.0) {
+        const double target = __dmul_rn(a.param, acc);
+        double c = 0.0;
+        L = P;
         for (int e = 0; e < P; ++e) {
           const int id = ids[e];
           const double supp = id < 2 * n - 1 ? (double)(n - abs(id - (n - 1))) : (double)n;
-          acc = __dadd_rn(acc, __dmul_rn(fmax(keys[e], 0.0), supp));
-        }
-        if (acc > 0.0) {
-          const double target = __dmul_rn(a.param, acc);
-          double c = 0.0;
-          L = P;
-          for (int e = 0; e < P; ++e) {
-            const int id = ids[e];
-            const double supp = id < 2 * n - 1 ? (double)(n - abs(id - (n - 1))) : (double)n;
-            c = __dadd_rn(c, __dmul_rn(fmax(keys[e], 0.0), supp));
-            if (c >= target) {
-              L = e + 1;
-              break;
-            }
+          c = __dadd_rn(c, __dmul_rn(fmax(keys[e], 0.0), supp));
+          if (c >= target) {
+            L = e + 1;
+            break;
           }
         }
       }
-      sel_len = L;
     }
-    __syncthreads();
-    for (int e = t; e < sel_len; e += blockDim.x) sel[ids[e]] = 1;
+    sel_len = L;
   }
   __syncthreads();
+  for (int e = t; e < P; e += blockDim.x) sel[e] = 0;
+  __syncthreads();
+  for (int e = t; e < sel_len; e += blockDim.x) sel[ids[e]] = 1;
+}
 
-  // 3. mask rows -> counts
-  const unsigned char* selC = sel;            // [2n-1], index j - i + n - 1
-  const unsigned char* selD = sel + 2 * n - 1;
-  const uint8_t* keep = a.keep ? a.keep + bh * a.F : nullptr;
-  const int warp = t / 32, lane = t % 32, nwarps = blockDim.x / 32;
-  auto pass = [&](int i, int j) -> bool {
+constexpr int kRowsPerCta = 32;   // 8 warps x 4 rows
+
+struct RowCtx {
+  const uint8_t* selC;   // smem [2n-1], index j - i + n - 1
+  const uint8_t* selD;   // smem [n]
+  const uint8_t* keep;   // global [F] or null
+  const int* frame_ab;
+  const int* row_frames;
+  int n, prefix_last, diag_guard;
+  __device__ __forceinline__ bool pass(int i, int j) const {
     if (selC[j - i + n - 1] || selD[j]) return true;
-    if (a.diag_guard && i == j) return true;
-    if (i <= a.prefix_last || j <= a.prefix_last) return true;
+    if (diag_guard && i == j) return true;
+    if (i <= prefix_last || j <= prefix_last) return true;
     if (keep) {
-      const int rlo = a.row_frames[2 * i], rhi = a.row_frames[2 * i + 1];
+      const int rlo = row_frames[2 * i], rhi = row_frames[2 * i + 1];
       for (int r = rlo; r <= rhi; ++r)
-        if (keep[r] && a.frame_ab[2 * r] <= j && j <= a.frame_ab[2 * r + 1]) return true;
+        if (keep[r] && frame_ab[2 * r] <= j && j <= frame_ab[2 * r + 1]) return true;
     }
     return false;
-  };
-  for (int i = warp; i < n; i += nwarps) {
-    int c = 0;
+  }
+};
+
+__device__ __forceinline__ RowCtx load_row_ctx(const PredictArgs& a, uint8_t* s_sel, size_t bh) {
+  const int P = 3 * a.n - 1;
+  const uint8_t* g = a.sel + bh * P;
+  for (int e = threadIdx.x; e < P; e += blockDim.x) s_sel[e] = g[e];
+  __syncthreads();
+  RowCtx c;
+  c.selC = s_sel;
+  c.selD = s_sel + 2 * a.n - 1;
+  c.keep = a.keep ? a.keep + bh * a.F : nullptr;
+  c.frame_ab = a.frame_ab;
+  c.row_frames = a.row_frames;
+  c.n = a.n;
+  c.prefix_last = a.prefix_last;
+  c.diag_guard = a.diag_guard;
+  return c;
+}
+
+// 2. passing blocks per row (warp per row, ballot + popc)
+__global__ void __launch_bounds__(256) count_kernel(PredictArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const size_t bh = blockIdx.y;
+  const RowCtx c = load_row_ctx(a, smem, bh);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, n = a.n;
+  for (int r = 0; r < kRowsPerCta / 8; ++r) {
+    const int i = blockIdx.x * kRowsPerCta + warp * (kRowsPerCta / 8) + r;
+    if (i >= n) break;
+    int cnt = 0;
     for (int j0 = 0; j0 < n; j0 += 32) {
       const int j = j0 + lane;
-      const unsigned m = __ballot_sync(0xffffffffu, j < n && pass(i, j));
-      c += __popc(m);
+      cnt += __popc(__ballot_sync(0xffffffffu, j < n && c.pass(i, j)));
     }
-    if (lane == 0) cnt[i] = c;
+    if (lane == 0) a.cnt[bh * n + i] = cnt;
   }
+}
+
+// 3. row pointers (prefix over the counts) and ascending column lists
+__global__ void __launch_bounds__(256) write_kernel(PredictArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int red[8];
+  __shared__ int rowoff[kRowsPerCta + 1];
+  const size_t bh = blockIdx.y;
+  const RowCtx c = load_row_ctx(a, smem, bh);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, n = a.n;
+  const int i0 = blockIdx.x * kRowsPerCta;
+  const int* cnt = a.cnt + bh * n;
+  int partial = 0;   // rows before this chunk
+  for (int i = threadIdx.x; i < i0; i += blockDim.x) partial += cnt[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) partial += __shfl_xor_sync(0xffffffffu, partial, o);
+  if (lane == 0) red[warp] = partial;
   __syncthreads();
-  // exclusive scan of cnt[0..n) -> row_ptr (block-wide: 2 rows per thread, n <= 2048)
-  {
-    const int i0 = 2 * t;
-    const int v0 = i0 < n ? cnt[i0] : 0, v1 = i0 + 1 < n ? cnt[i0 + 1] : 0;
-    int s = v0 + v1;
-    int incl = s;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (lane == 31) warp_tot[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-      int w = lane < nwarps ? warp_tot[lane] : 0;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, w, o);
-        if (lane >= o) w += y;
-      }
-      warp_tot[lane] = w;  // inclusive
-    }
-    __syncthreads();
-    const int base = (warp > 0 ? warp_tot[warp - 1] : 0) + incl - s;
-    __syncthreads();
-    if (i0 < n) cnt[i0] = base;
-    if (i0 + 1 < n) cnt[i0 + 1] = base + v0;
-    if (t == 0) cnt[n] = warp_tot[31];
+  if (threadIdx.x == 0) {
+    int base = 0;
+    for (int w = 0; w < 8; ++w) base += red[w];
+    rowoff[0] = base;
+    for (int r = 0; r < kRowsPerCta; ++r) rowoff[r + 1] = rowoff[r] + (i0 + r < n ? cnt[i0 + r] : 0);
   }
   __syncthreads();
   int* rp = a.row_ptr + bh * (n + 1);
-  for (int i = t; i <= n; i += blockDim.x) rp[i] = cnt[i];
+  for (int r = threadIdx.x; r <= kRowsPerCta; r += blockDim.x) {
+    const int i = i0 + r;
+    if (i <= n && (r < kRowsPerCta || i == n)) rp[i] = rowoff[r];
+  }
   int* ci = a.col_idx + bh * (size_t)n * n;
-  for (int i = warp; i < n; i += nwarps) {
-    int pos = cnt[i];
+  for (int r = 0; r < kRowsPerCta / 8; ++r) {
+    const int rr = warp * (kRowsPerCta / 8) + r;
+    const int i = i0 + rr;
+    if (i >= n) break;
+    int pos = rowoff[rr];
     for (int j0 = 0; j0 < n; j0 += 32) {
       const int j = j0 + lane;
-      const bool ps = j < n && pass(i, j);
+      const bool ps = j < n && c.pass(i, j);
       const unsigned m = __ballot_sync(0xffffffffu, ps);
       if (ps) ci[pos + __popc(m & ((1u << lane) - 1u))] = j;
       pos += __popc(m);
@@ -204,11 +233,10 @@ extern "C" mod_status mod_predict_block_mask(mod_plan P, const double* x_prev, c
                                              int32_t t_curr, int32_t t, const uint8_t* keep,
                                              const mod_selection* sel, int32_t* row_ptr, int32_t* col_idx,
                                              void* ws, void* stream) {
-  (void)ws;
   mod_status st = mod_validate_plan(P);
   if (st != MOD_OK) return st;
-  MOD_REQUIRE(x_prev && x_curr && row_ptr && col_idx, MOD_ERR_USAGE,
-              "mod_predict_block_mask: x_prev, x_curr, row_ptr, col_idx must be non-NULL");
+  MOD_REQUIRE(x_prev && x_curr && row_ptr && col_idx && ws, MOD_ERR_USAGE,
+              "mod_predict_block_mask: x_prev, x_curr, row_ptr, col_idx, ws must be non-NULL");
   MOD_REQUIRE(t_prev != t_curr, MOD_ERR_INPUT, "mod_predict_block_mask: t_prev == t_curr == %d (zero denominator)",
               t_curr);
   PredictArgs a;
@@ -231,15 +259,24 @@ extern "C" mod_status mod_predict_block_mask(mod_plan P, const double* x_prev, c
   a.diag_guard = P->cfg.diag_guard;
   a.dt_hist = (double)(t_curr - t_prev);
   a.dt_pred = (double)(t - t_curr);
+  a.sel = reinterpret_cast<uint8_t*>(static_cast<char*>(ws) + P->ws_sel);
+  a.cnt = reinterpret_cast<int*>(static_cast<char*>(ws) + P->ws_cnt);
   int P2 = 1;
   while (P2 < 3 * P->n - 1) P2 <<= 1;
   a.P2 = P2;
-  const size_t smem = (size_t)P2 * (sizeof(double) + sizeof(int)) + (P->n + 1) * sizeof(int) + 3 * P->n + 16;
-  MOD_CUDA(cudaFuncSetAttribute(predict_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const size_t smem = (size_t)P2 * (sizeof(double) + sizeof(int));
+  MOD_CUDA(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int BH = P->L.batch * P->L.heads;
-  predict_kernel<<<BH, 1024, smem, as_stream(stream)>>>(a);
+  cudaStream_t s = as_stream(stream);
+  select_kernel<<<BH, 1024, smem, s>>>(a);
   MOD_LAUNCH_CHECK();
-  mod_note_launches(1);
+  const dim3 rg((P->n + kRowsPerCta - 1) / kRowsPerCta, BH);
+  const size_t rsm = (size_t)(3 * P->n + 16);
+  count_kernel<<<rg, 256, rsm, s>>>(a);
+  MOD_LAUNCH_CHECK();
+  write_kernel<<<rg, 256, rsm, s>>>(a);
+  MOD_LAUNCH_CHECK();
+  mod_note_launches(3);
   return MOD_OK;
 }
 
