@@ -233,7 +233,7 @@ def run_ours(args):
             ev["attn"].append((e[1], e[2]))
             ev["rest"].append((e[0], e[1], e[2], e[3]))
 
-    launches_per_step = 3 + 1 + 2 + 5          # predict (select, count, write) + attn + stats (2) + update (5)
+    launches_per_step = 3 + 1 + 2 + 6          # predict (select, count, write) + attn + stats (2) + update (6)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()

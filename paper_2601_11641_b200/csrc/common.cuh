@@ -54,7 +54,7 @@ struct mod_plan_s {
   double* d_ginv;               // device [p*p] deflated Gram inverse
   size_t ws_bytes;
   // workspace carve (byte offsets)
-  size_t ws_qbar, ws_kbar, ws_part, ws_r, ws_x, ws_nae, ws_sel, ws_cnt;
+  size_t ws_qbar, ws_kbar, ws_part, ws_r, ws_x, ws_nae, ws_sel, ws_cnt, ws_solve;
   int proj_tiles;               // row tiles of the projection kernel
   int sm_count;
   double min_pivot;             // smallest Gauss-Jordan pivot of the deflated Gram

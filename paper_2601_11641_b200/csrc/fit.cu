@@ -64,29 +64,55 @@ __global__ void reduce_rhs_kernel(const double* __restrict__ part, double* __res
   r[e] = s;
 }
 
-constexpr int KR = 8, BB = 32, LC = 128;
-__global__ void __launch_bounds__(256) solve_kernel(const double* __restrict__ Ginv, const double* __restrict__ r,
-                                                    double* __restrict__ X, int p, int BH) {
-  __shared__ double Gs[KR][LC];
-  __shared__ double Rs[BB][LC + 1];
-  const int k0 = blockIdx.x * KR, b0 = blockIdx.y * BB;
-  const int t = threadIdx.x, kk = t / 32, bb = t % 32;
-  double acc = 0.0;
-  for (int l0 = 0; l0 < p; l0 += LC) {
+// X[bh][k] = sum_l G'^-1[k][l] r[bh][l] as a split-K GEMM: CTA (32 rows k, 32 heads, one l segment),
+// 64 threads with 4 x 4 register tiles over shared-memory chunks of 32 l; partial sums go to a
+// [segments, BH, p] buffer that solve_reduce_kernel adds in fixed order (deterministic, no atomics).
+constexpr int SK_SEG = 8, SK_T = 32, SK_L = 32;
+__global__ void __launch_bounds__(64) solve_partial_kernel(const double* __restrict__ Ginv, const double* __restrict__ r,
+                                                           double* __restrict__ part, int p, int BH, int seg_len) {
+  __shared__ double Gs[SK_L][SK_T + 1];   // [l][k]
+  __shared__ double Rs[SK_L][SK_T + 1];   // [l][bh]
+  const int k0 = blockIdx.x * SK_T, b0 = blockIdx.y * SK_T, seg = blockIdx.z;
+  const int lbeg = seg * seg_len, lend = min(p, lbeg + seg_len);
+  const int t = threadIdx.x, tk = t / 8, tb = t % 8;      // rows k0+4tk.., heads b0+tb+8m
+  double acc[4][4] = {};
+  for (int l0 = lbeg; l0 < lend; l0 += SK_L) {
     __syncthreads();
-    for (int e = t; e < KR * LC; e += 256) {
-      const int a = e / LC, l = e % LC;
-      Gs[a][l] = (k0 + a < p && l0 + l < p) ? Ginv[(size_t)(k0 + a) * p + l0 + l] : 0.0;
-    }
-    for (int e = t; e < BB * LC; e += 256) {
-      const int a = e / LC, l = e % LC;
-      Rs[a][l] = (b0 + a < BH && l0 + l < p) ? r[(size_t)(b0 + a) * p + l0 + l] : 0.0;
+    for (int e = t; e < SK_T * SK_L; e += 64) {
+      const int a = e / SK_L, l = e % SK_L;               // coalesced along l
+      Gs[l][a] = (k0 + a < p && l0 + l < lend) ? Ginv[(size_t)(k0 + a) * p + l0 + l] : 0.0;
+      Rs[l][a] = (b0 + a < BH && l0 + l < lend) ? r[(size_t)(b0 + a) * p + l0 + l] : 0.0;
     }
     __syncthreads();
-#pragma unroll 8
-    for (int l = 0; l < LC; ++l) acc = fma(Gs[kk][l], Rs[bb][l], acc);
+#pragma unroll 4
+    for (int l = 0; l < SK_L; ++l) {
+      double g[4], rv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        g[i] = Gs[l][tk * 4 + i];
+        rv[i] = Rs[l][tb + 8 * i];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int m = 0; m < 4; ++m) acc[i][m] = fma(g[i], rv[m], acc[i][m]);
+    }
   }
-  if (k0 + kk < p && b0 + bb < BH) X[(size_t)(b0 + bb) * p + k0 + kk] = acc;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int k = k0 + tk * 4 + i, b = b0 + tb + 8 * m;
+      if (k < p && b < BH) part[((size_t)seg * BH + b) * p + k] = acc[i][m];
+    }
+}
+
+__global__ void solve_reduce_kernel(const double* __restrict__ part, double* __restrict__ X, int p, int BH, int nseg) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (size_t)BH * p) return;
+  double s = 0.0;
+  for (int g = 0; g < nseg; ++g) s += part[(size_t)g * BH * p + e];
+  X[e] = s;
 }
 
 // ||U - MX||^2 and ||U||^2 per (head, row tile)
@@ -183,7 +209,7 @@ __global__ void roll_kernel(double* __restrict__ x_prev, double* __restrict__ x_
   x_curr[e] = X[e];
 }
 
-// r = M^T vec U for every head, then X = G'^{-1} r.  3 launches.
+// r = M^T vec U for every head, then X = G'^{-1} r.  4 launches.
 mod_status fit_from_map(mod_plan P, const float* U, double* X, void* ws, cudaStream_t s) {
   const int BH = P->L.batch * P->L.heads, n = P->n, p = P->p, tiles = P->proj_tiles;
   double* part = reinterpret_cast<double*>(static_cast<char*>(ws) + P->ws_part);
@@ -193,7 +219,12 @@ mod_status fit_from_map(mod_plan P, const float* U, double* X, void* ws, cudaStr
   const size_t tot = (size_t)BH * p;
   reduce_rhs_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(part, r, p, tiles, BH);
   MOD_LAUNCH_CHECK();
-  solve_kernel<<<dim3((p + KR - 1) / KR, (BH + BB - 1) / BB), 256, 0, s>>>(P->d_ginv, r, X, p, BH);
+  const int seg_len = ((p + SK_SEG - 1) / SK_SEG + SK_L - 1) / SK_L * SK_L;
+  double* spart = reinterpret_cast<double*>(static_cast<char*>(ws) + P->ws_solve);
+  solve_partial_kernel<<<dim3((p + SK_T - 1) / SK_T, (BH + SK_T - 1) / SK_T, SK_SEG), 64, 0, s>>>(P->d_ginv, r, spart, p,
+                                                                                             BH, seg_len);
+  MOD_LAUNCH_CHECK();
+  solve_reduce_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(spart, X, p, BH, SK_SEG);
   MOD_LAUNCH_CHECK();
   return MOD_OK;
 }
@@ -207,7 +238,7 @@ extern "C" mod_status mod_fit_mixture(mod_plan P, const float* stats, double* x,
   cudaStream_t s = as_stream(stream);
   st = fit_from_map(P, stats, x, ws, s);
   if (st != MOD_OK) return st;
-  int launches = 3;
+  int launches = 4;
   if (nae) {
     const int BH = P->L.batch * P->L.heads, tiles = P->proj_tiles;
     double* part = reinterpret_cast<double*>(static_cast<char*>(ws) + P->ws_nae);
@@ -252,6 +283,6 @@ extern "C" mod_status mod_update_online_mask(mod_plan P, const float* stats_fres
   const size_t tot = (size_t)BH * P->p;
   roll_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(x_prev, x_curr, X, tot);
   MOD_LAUNCH_CHECK();
-  mod_note_launches(5);
+  mod_note_launches(6);
   return MOD_OK;
 }

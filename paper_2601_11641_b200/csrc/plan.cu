@@ -322,6 +322,7 @@ extern "C" mod_status mod_plan_create(const mod_layout* layout, const mod_config
   P->ws_nae = off;  off = align_up(off + 2 * BH * (size_t)n * sizeof(double));
   P->ws_sel = off;  off = align_up(off + BH * (size_t)(3 * n));
   P->ws_cnt = off;  off = align_up(off + BH * (size_t)n * sizeof(int));
+  P->ws_solve = off; off = align_up(off + 8 * BH * (size_t)p * sizeof(double));
   P->ws_bytes = off;
   cudaSetDevice(prev_dev);
   *out = P;

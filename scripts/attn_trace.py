@@ -24,7 +24,7 @@ ev = sorted((buf[2 * i], buf[2 * i + 1] >> 32, buf[2 * i + 1] & 0xffffffff) for 
 n = len(ev)
 t0 = ev[0][0]
 names = {1: "P:k_empty", 2: "P:v_empty", 10: "M:k_full", 11: "M:S_issued", 12: "M:p_full", 13: "M:v_full", 14: "M:PV_issued",
-         20: "S0:s_full", 21: "S1:s_full", 30: "S0:exp_done", 31: "S1:exp_done", 40: "S0:p_arrive", 41: "S1:p_arrive"}
+         20: "S0:s_full", 21: "S1:s_full", 30: "S0:exp_done", 31: "S1:exp_done", 40: "S0:p_arrive", 41: "S1:p_arrive", 50: "S0:ld_done", 51: "S1:ld_done", 60: "S0:max_xchg", 61: "S1:max_xchg"}
 with open("gpurun_out/trace.txt", "w") as f:
     for t, tag, j in ev:
         f.write(f"{t - t0:9d} {names.get(tag, tag):14s} j={j}\n")
