@@ -201,7 +201,19 @@ def run_ours(args):
     q1, k1, _ = syn.family_s(w, step=M_WARMUP - 1, **gen)
     W1 = P.collect_block_stats(q1, k1)
     del q1, k1
-    q, k, v = syn.family_s(w, step=M_WARMUP, **gen)
+    seq = None
+    if args.ulysses:
+        # config 5: activations arrive sequence-sharded [B, N/P, H, D]; the step starts with the Ulysses
+        # all-to-all to head shards and ends with the inverse (NCCL all_to_all_single over NVLink)
+        from paper_2601_11641_b200.parallel import heads_to_seq, seq_to_heads
+        assert w_full.tokens % ws == 0, "tokens not divisible by world size"
+        full = syn.family_s(w_full, step=M_WARMUP, seed=syn.SEED_BASE, device="cuda")
+        Ns = w_full.tokens // ws
+        seq = [t.permute(0, 2, 1, 3)[:, rank * Ns:(rank + 1) * Ns].contiguous() for t in full]
+        del full
+        q, k, v = (seq_to_heads(t) for t in seq)
+    else:
+        q, k, v = syn.family_s(w, step=M_WARMUP, **gen)
     W2 = P.collect_block_stats(q, k)
     x_prev0, x_curr0 = P.fit_mixture(W1), P.fit_mixture(W2)
     keep = P.keep_frames(x_prev0, x_curr0)
@@ -217,6 +229,9 @@ def run_ours(args):
     ev = {k_: [] for k_ in ("attn", "rest")}
 
     def step(timed_kernels=False):
+        if seq is not None:
+            for dst, src in zip((q, k, v), seq):
+                dst.copy_(seq_to_heads(src))
         if timed_kernels:
             e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
             e[0].record(stream)
@@ -228,6 +243,8 @@ def run_ours(args):
             e[2].record(stream)
         P.collect_block_stats(q, k, out=Wf)
         P.update_online_mask(Wf, rp, ci, hist, xs_prev, xs_curr)
+        if seq is not None:
+            step.o_seq = heads_to_seq(o)
         if timed_kernels:
             e[3].record(stream)
             ev["attn"].append((e[1], e[2]))
@@ -327,7 +344,7 @@ def run_ours(args):
                    "target_sparsity": args.sparsity, "nnz_blocks_rank0": nnz_local,
                    "step": "predict(K2b) + attn(K4) + stats(K1) + update(K3: Eq.5 + fit K2a + roll) at t_p=22",
                    "l2": "inputs larger than L2 (Q,K,V = %.2f GB per rank > 126 MB)" % (3 * q.numel() * 2 / 1e9),
-                   "parallelism": f"head-parallel x{ws}"},
+                   "parallelism": (f"ulysses a2a + head-parallel x{ws}" if args.ulysses else f"head-parallel x{ws}")},
         "attn_ms": round(attn_ms_max, 3), "attn_tflops": round(attn_tflops, 1),
         "attn_pct_bf16_peak": round(100 * attn_tflops / burst, 1),
         "pipeline_overhead_ms": {"predict": round(pred_ms, 4), "stats_update": round(upd_ms, 4)},
@@ -442,6 +459,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-blocks", type=int, default=4)
+    ap.add_argument("--ulysses", action="store_true",
+                    help="sequence-sharded inputs: Ulysses all-to-all in and out of every step (config 5)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

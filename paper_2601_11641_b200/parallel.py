@@ -35,12 +35,18 @@ def lpt_head_assignment(cost, world: int) -> list[list[int]]:
     return [sorted(x) for x in out]
 
 
+def _world(group) -> int:
+    return dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+
+
 def seq_to_heads(x_seq: torch.Tensor, group=None) -> torch.Tensor:
     """Ulysses forward all-to-all: sequence shard [B, N/P, H, D] -> head shard [B, H/P, N, D] (contiguous).
 
     Rank r holds tokens [r*N/P, (r+1)*N/P) of every head; afterwards it holds every token of heads
-    [r*H/P, (r+1)*H/P).  One all_to_all_single per tensor."""
-    P = dist.get_world_size(group)
+    [r*H/P, (r+1)*H/P).  One all_to_all_single per tensor (a local permute when P = 1)."""
+    P = _world(group)
+    if P == 1:
+        return x_seq.permute(0, 2, 1, 3).contiguous()
     B, Ns, H, D = x_seq.shape
     if H % P:
         raise ValueError(f"heads={H} not divisible by world size {P}")
@@ -54,7 +60,9 @@ def seq_to_heads(x_seq: torch.Tensor, group=None) -> torch.Tensor:
 
 def heads_to_seq(x_head: torch.Tensor, group=None) -> torch.Tensor:
     """Ulysses inverse all-to-all: head shard [B, H/P, N, D] -> sequence shard [B, N/P, H, D]."""
-    P = dist.get_world_size(group)
+    P = _world(group)
+    if P == 1:
+        return x_head.permute(0, 2, 1, 3).contiguous()
     B, Hp, N, D = x_head.shape
     if N % P:
         raise ValueError(f"tokens={N} not divisible by world size {P}")
