@@ -158,6 +158,16 @@ mod_status mod_block_sparse_attn_fwd(mod_plan plan, const void* q, const void* k
                                      const int32_t* row_ptr, const int32_t* col_idx, void* o, float* lse,
                                      void* ws, void* stream);
 
+/* EXACT statistic (Eq. 2) in informativeness polarity (reading Z3):
+ * for every block (i,j) listed in the CSR, stats[b,h,i,j] = 1 - S_ij with
+ *   S_ij = #{(p,q) in I_i x I_j : exp(s Q_p.K_q - lse_p) < eta} / (|I_i||I_j|)   (strict <),
+ * lse: fp32 [B,H,N] natural-log row normalisers -- from mod_block_sparse_attn_fwd on the dense list
+ * (warm-up, full map) or on the sparse list (Eq. 5's A_masked renormalised over the kept blocks).
+ * Unlisted entries of stats are left untouched.  eta in (0,1) (1e-4, App. A). */
+mod_status mod_collect_exact_sparsity(mod_plan plan, const void* q, const void* k, const float* lse,
+                                      const int32_t* row_ptr, const int32_t* col_idx, float eta, float* stats,
+                                      void* ws, void* stream);
+
 /* Dense mask helper (the warm-up's full attention, Alg. 1): all-ones CSR. */
 mod_status mod_fill_dense_mask(mod_plan plan, int32_t* row_ptr, int32_t* col_idx, void* stream);
 

@@ -82,3 +82,35 @@ def sparsity_from_map(A, L: Layout, eta: float = 1e-4):
 def informativeness_from_sparsity(S):
     """Reading Z3: U = 1 - S (larger = more informative)."""
     return 1.0 - np.asarray(S, dtype=np.float64)
+
+
+def exact_sparsity_masked(q, k, masks, L: Layout, eta: float = 1e-4, scale: float | None = None):
+    """Eq. 2 on the MASKED post-softmax map of sparse attention (Eq. 1; Eq. 5's A_masked with
+    reading Z12: normalised over the unmasked keys only).  Returns S [B,H,n,n] with NaN at the blocks
+    the mask removes (they keep their history in Eq. 5) and the log-sum-exp lse [B,H,N] of each row
+    over its unmasked keys."""
+    q = _f64(q)
+    k = _f64(k)
+    masks = np.asarray(masks, dtype=bool)
+    s = 1.0 / np.sqrt(L.head_dim) if not scale else float(scale)
+    B, H, N, _ = q.shape
+    n = L.n
+    tb = np.arange(N) // L.block
+    S = np.full((B, H, n, n), np.nan)
+    lse = np.zeros((B, H, N))
+    for b in range(B):
+        for h in range(H):
+            A = s * q[b, h] @ k[b, h].T
+            km = masks[b, h][tb][:, tb]
+            A = np.where(km, A, -np.inf)
+            m = A.max(axis=1, keepdims=True)
+            e = np.exp(A - m)
+            z = e.sum(axis=1, keepdims=True)
+            lse[b, h] = (m + np.log(z))[:, 0]
+            P = e / z                                              # masked, renormalised (Z12)
+            for i in range(n):
+                ilo, ihi = L.block_range(i)
+                for j in np.nonzero(masks[b, h, i])[0]:
+                    jlo, jhi = L.block_range(j)
+                    S[b, h, i, j] = (P[ilo:ihi, jlo:jhi] < eta).sum() / ((ihi - ilo) * (jhi - jlo))
+    return S, lse

@@ -62,6 +62,7 @@ SIGNATURES = {
     "mod_update_online_mask": (I32, [P, P, P, P, P, P, P, P, P]),
     "mod_block_sparse_attn_fwd": (I32, [P, P, P, P, P, P, P, P, P, P]),
     "mod_fill_dense_mask": (I32, [P, P, P, P]),
+    "mod_collect_exact_sparsity": (I32, [P, P, P, P, P, P, C.c_float, P, P, P]),
     "mod_last_launch_count": (I32, []),
 }
 

@@ -167,6 +167,14 @@ class Plan:
                                             _ptr(out), _ptr(lse), _ptr(self.workspace()), _stream()))
         return out, lse
 
+    def collect_exact_sparsity(self, q, k, lse, row_ptr, col_idx, eta: float = 1e-4, out=None):
+        """U = 1 - S of Eq. 2 for the listed blocks (unlisted entries of ``out`` untouched)."""
+        self._check_qkv(q, k)
+        out = self.empty_stats().fill_(float("nan")) if out is None else out
+        check(lib.mod_collect_exact_sparsity(self._h, _ptr(q), _ptr(k), _ptr(lse), _ptr(row_ptr), _ptr(col_idx),
+                                             eta, _ptr(out), _ptr(self.workspace()), _stream()))
+        return out
+
     def dense_mask(self, out=None):
         rp, ci = self.empty_mask() if out is None else out
         check(lib.mod_fill_dense_mask(self._h, _ptr(rp), _ptr(ci), _stream()))

@@ -345,3 +345,65 @@ def test_plan_errors(M):
     x = P.empty_x()
     with pytest.raises(M.ModditError, match="zero denominator"):
         P.predict_block_mask(x, x, 5, 5, 6)
+
+
+# ------------------------------------------------------------------------------------------ f1 EXACT statistic
+def _exact_check(Ug, S_ref, q, k, lse32, masks, L, eta):
+    """Blocks must agree except for probabilities within the fp32 evaluation band of eta."""
+    s = 1.0 / np.sqrt(L.head_dim)
+    qn, kn = q.double().cpu().numpy(), k.double().cpu().numpy()
+    tb = np.arange(L.N) // L.block
+    for b in range(masks.shape[0]):
+        for h in range(masks.shape[1]):
+            A = s * qn[b, h] @ kn[b, h].T - lse32[b, h][:, None]          # ln P with the kernel's lse
+            amb = np.abs(A - np.log(eta)) <= 1e-3                          # fp32 dot products + threshold
+            for i in range(L.n):
+                ilo, ihi = L.block_range(i)
+                for j in np.nonzero(masks[b, h, i])[0]:
+                    jlo, jhi = L.block_range(j)
+                    nb = amb[ilo:ihi, jlo:jhi].sum()
+                    tol = (nb + 0.5) / ((ihi - ilo) * (jhi - jlo))
+                    assert abs((1.0 - Ug[b, h, i, j]) - S_ref[b, h, i, j]) <= tol, (b, h, i, j)
+
+
+@pytest.mark.parametrize("w", [TINY, SMALL_PREFIX, COG_SMALL], ids=lambda w: w.name)
+def test_exact_sparsity_dense_and_masked(M, w):
+    L = olayout(w)
+    P = plan_for(M, w)
+    q, k, v = syn.family_s(w, device="cuda")
+    eta = 1e-4
+    # dense (warm-up): lse of the full attention
+    ones = np.ones((w.batch, w.heads, L.n, L.n), dtype=bool)
+    S_ref, lse_ref = O.exact_sparsity_masked(q.cpu(), k.cpu(), ones, L, eta)
+    lse32 = torch.from_numpy(lse_ref.astype(np.float32)).cuda()
+    rp, ci = P.dense_mask()
+    U = P.collect_exact_sparsity(q, k, lse32, rp, ci, eta)
+    torch.cuda.synchronize()
+    _exact_check(U.double().cpu().numpy(), S_ref, q, k, lse32.double().cpu().numpy(), ones, L, eta)
+    assert np.allclose(S_ref, O.exact_sparsity(q.cpu(), k.cpu(), L, eta))
+    # masked (re-estimation step): lse over the kept blocks, unlisted entries untouched
+    masks = _random_masks(w, L, 0.3, 71)
+    S_m, lse_m = O.exact_sparsity_masked(q.cpu(), k.cpu(), masks, L, eta)
+    lse32 = torch.from_numpy(lse_m.astype(np.float32)).cuda()
+    rp, ci = masks_to_csr(masks)
+    U2 = P.collect_exact_sparsity(q, k, lse32, rp, ci, eta)
+    torch.cuda.synchronize()
+    U2n = U2.double().cpu().numpy()
+    assert np.all(np.isnan(U2n[~masks]))
+    _exact_check(U2n, S_m, q, k, lse32.double().cpu().numpy(), masks, L, eta)
+
+
+def test_exact_sparsity_with_kernel_lse(M):
+    """End to end on the GPU: K4's own lse (sparse) feeds the EXACT statistic."""
+    w = SMALL_PREFIX
+    L = olayout(w)
+    P = plan_for(M, w)
+    q, k, v = syn.family_s(w, device="cuda")
+    masks = _random_masks(w, L, 0.4, 72)
+    rp, ci = masks_to_csr(masks)
+    _, lse = P.block_sparse_attn_fwd(q, k, v, rp, ci)
+    U = P.collect_exact_sparsity(q, k, lse, rp, ci, 1e-4)
+    torch.cuda.synchronize()
+    S_m, _ = O.exact_sparsity_masked(q.cpu(), k.cpu(), masks, L, 1e-4)
+    d = np.abs((1 - U.double().cpu().numpy()[masks]) - S_m[masks])
+    assert d.max() <= 0.02 and d.mean() <= 1e-3      # K4 lse error (<= 5e-3) moves a few threshold decisions

@@ -81,3 +81,27 @@ def test_sparsity_monotone_in_eta():
         if prev is not None:
             assert np.all(prev <= S)
         prev = S
+
+
+def test_masked_exact_sparsity_all_ones_equals_dense():
+    L = _lay()
+    rng = np.random.default_rng(4)
+    q = rng.standard_normal((1, 2, L.N, 8)) * 2
+    k = rng.standard_normal((1, 2, L.N, 8)) * 2
+    ones = np.ones((1, 2, L.n, L.n), dtype=bool)
+    Sm, lse = O.exact_sparsity_masked(q, k, ones, L, 1e-3)
+    assert np.array_equal(Sm, O.exact_sparsity(q, k, L, 1e-3))
+    from scipy.special import logsumexp
+    assert np.allclose(lse, logsumexp(q @ np.swapaxes(k, -1, -2) / np.sqrt(8), axis=-1), atol=1e-12)
+
+
+def test_masked_exact_sparsity_renormalises_over_selection():
+    L = _lay()
+    rng = np.random.default_rng(5)
+    q = rng.standard_normal((1, 1, L.N, 8))
+    k = rng.standard_normal((1, 1, L.N, 8))
+    m = np.zeros((1, 1, L.n, L.n), dtype=bool)
+    m[0, 0, :, 0] = True                     # a single key block per row: uniform-ish P over it
+    Sm, _ = O.exact_sparsity_masked(q, k, m, L, 1e-9)
+    assert np.all(np.isnan(Sm[0, 0, :, 1:]))
+    assert np.all(Sm[0, 0, :, 0] == 0.0)     # no probability over a single 4-key block falls below 1e-9
