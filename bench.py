@@ -195,12 +195,30 @@ def run_ours(args):
     D, N, blk = w.head_dim, w.tokens, w.block
     burst, sustained, hbm, peak_src = load_peaks()
 
-    P = Plan(w, top_k=1, tau_e=0.0)
+    exact = args.stat == "exact"
+    P = Plan(w, top_k=1, tau_e=0.0, masked_renorm=not exact)
     gen = dict(seed=syn.SEED_BASE, device="cuda", head_offset=h0, total_heads=w_full.heads)
+    extra = {}
+
+    def warm_stat(qq, kk, vv):
+        """Statistic of a warm-up step: POOLED, or EXACT Eq. 2 from the dense attention's lse."""
+        if not exact:
+            return P.collect_block_stats(qq, kk)
+        rpd, cid = P.dense_mask()
+        _, lsed = P.block_sparse_attn_fwd(qq, kk, vv, rpd, cid)
+        torch.cuda.synchronize()
+        e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e_a.record()
+        U = P.collect_exact_sparsity(qq, kk, lsed, rpd, cid, args.eta)
+        e_b.record()
+        torch.cuda.synchronize()
+        extra["exact_dense_stat_ms"] = round(e_a.elapsed_time(e_b), 3)
+        return U
+
     # ---- warm-up phase of Alg. 1 (P:992-1002): statistics at t = m-1 and t = m, fits, keep decision
-    q1, k1, _ = syn.family_s(w, step=M_WARMUP - 1, **gen)
-    W1 = P.collect_block_stats(q1, k1)
-    del q1, k1
+    q1, k1, v1 = syn.family_s(w, step=M_WARMUP - 1, **gen)
+    W1 = warm_stat(q1, k1, v1)
+    del q1, k1, v1
     seq = None
     if args.ulysses:
         # config 5: activations arrive sequence-sharded [B, N/P, H, D]; the step starts with the Ulysses
@@ -214,7 +232,7 @@ def run_ours(args):
         q, k, v = (seq_to_heads(t) for t in seq)
     else:
         q, k, v = syn.family_s(w, step=M_WARMUP, **gen)
-    W2 = P.collect_block_stats(q, k)
+    W2 = warm_stat(q, k, v)
     x_prev0, x_curr0 = P.fit_mixture(W1), P.fit_mixture(W2)
     keep = P.keep_frames(x_prev0, x_curr0)
     hist = W2.clone()                                  # A_hat^(t_p^(0)) = A^(m)
@@ -241,7 +259,10 @@ def run_ours(args):
         P.block_sparse_attn_fwd(q, k, v, rp, ci, out=o, lse=lse)
         if timed_kernels:
             e[2].record(stream)
-        P.collect_block_stats(q, k, out=Wf)
+        if exact:   # Eq. 2 on the masked map of this step (lse over the kept blocks, reading Z12)
+            P.collect_exact_sparsity(q, k, lse, rp, ci, args.eta, out=Wf)
+        else:
+            P.collect_block_stats(q, k, out=Wf)
         P.update_online_mask(Wf, rp, ci, hist, xs_prev, xs_curr)
         if seq is not None:
             step.o_seq = heads_to_seq(o)
@@ -250,7 +271,7 @@ def run_ours(args):
             ev["attn"].append((e[1], e[2]))
             ev["rest"].append((e[0], e[1], e[2], e[3]))
 
-    launches_per_step = 3 + 1 + 2 + 6          # predict (select, count, write) + attn + stats (2) + update (6)
+    launches_per_step = 3 + 1 + (1 if exact else 2) + 6   # predict (3) + attn + statistic + update (6)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -352,7 +373,7 @@ def run_ours(args):
         "dense_tflops_fastest": round(dense_flops / (fastest * 1e-3) / 1e12, 1) if fastest else None,
         "speedup_vs_fastest_dense": round(fastest / attn_ms, 3) if fastest else None,
         "roofline": roof, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
-        "clocks": clk.summary(), "library": mod.LIB_PATH,
+        "clocks": clk.summary(), "library": mod.LIB_PATH, "statistic": args.stat, **extra,
     })
 
     # ---- cpu baseline: the oracle as it stands on a bounded sample (rank 0, N=1 only)
@@ -459,6 +480,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-blocks", type=int, default=4)
+    ap.add_argument("--stat", default="pooled", choices=["pooled", "exact"],
+                    help="block statistic: pooled (north_star (1)) or the paper's exact Eq. 2 (SURVEY f1)")
+    ap.add_argument("--eta", type=float, default=1e-4)
     ap.add_argument("--ulysses", action="store_true",
                     help="sequence-sharded inputs: Ulysses all-to-all in and out of every step (config 5)")
     args = ap.parse_args()

@@ -32,10 +32,17 @@ class ScheduleState:
 
 class Schedule:
     def __init__(self, plan: Plan, T: int = 50, m: int = 12, dt: int = 10, top_k: int | None = None,
-                 select_mode: int | None = None, select_param: float | None = None):
+                 select_mode: int | None = None, select_param: float | None = None, stat: str = "pooled",
+                 eta: float = 1e-4):
         if not (1 <= m < T) or dt < 1 or m < 2:
             raise ValueError(f"bad schedule T={T} m={m} dt={dt}")
+        if stat not in ("pooled", "exact"):
+            raise ValueError(f"stat={stat!r} must be 'pooled' or 'exact'")
+        if stat == "exact" and plan.config["masked_renorm"]:
+            raise ValueError("stat='exact' needs a Plan with masked_renorm=False: the masked map is already "
+                             "renormalised by the sparse attention's lse (reading Z12)")
         self.P, self.T, self.m, self.dt = plan, T, m, dt
+        self.stat, self.eta = stat, eta
         self.sel = dict(top_k=top_k, select_mode=select_mode, select_param=select_param)
         self.state = ScheduleState()
         self._dense = None
@@ -51,6 +58,7 @@ class Schedule:
         return self._dense
 
     def step(self, t: int, q, k, v, out=None, lse=None):
+        """One denoising step of one attention layer; returns (O, lse)."""
         P, S = self.P, self.state
         if not 1 <= t <= self.T:
             raise ValueError(f"t={t} outside [1, {self.T}]")
@@ -58,10 +66,10 @@ class Schedule:
             rp, ci = self.dense_mask()
             o, l = P.block_sparse_attn_fwd(q, k, v, rp, ci, out=out, lse=lse)
             if t == self.m - 1:
-                S.W_warm = P.collect_block_stats(q, k)
+                S.W_warm = self._stat(q, k, l, rp, ci)
                 S.x_prev, S.t_prev = P.fit_mixture(S.W_warm), t
             elif t == self.m:
-                W = P.collect_block_stats(q, k)
+                W = self._stat(q, k, l, rp, ci)
                 S.x_curr, S.t_curr = P.fit_mixture(W), t
                 S.keep = P.keep_frames(S.x_prev, S.x_curr)
                 S.hist = W                                    # A_hat^(t_p^(0)) = A^(m)
@@ -71,11 +79,18 @@ class Schedule:
         rp, ci = P.predict_block_mask(S.x_prev, S.x_curr, S.t_prev, S.t_curr, t, S.keep, **self.sel)
         o, l = P.block_sparse_attn_fwd(q, k, v, rp, ci, out=out, lse=lse)
         if self.is_update_step(t):
-            W = P.collect_block_stats(q, k)
+            W = self._stat(q, k, l, rp, ci)
             P.update_online_mask(W, rp, ci, S.hist, S.x_prev, S.x_curr)
             S.t_prev, S.t_curr = S.t_curr, t
         self.last_mask = (rp, ci)
         return o, l
+
+    def _stat(self, q, k, lse, rp, ci):
+        """Block statistic U of this step: POOLED (north_star (1)) or EXACT Eq. 2 from the attention's lse
+        over the listed blocks (dense list at warm-up, sparse list at t_p: Eq. 5's A_masked)."""
+        if self.stat == "pooled":
+            return self.P.collect_block_stats(q, k)
+        return self.P.collect_exact_sparsity(q, k, lse, rp, ci, self.eta)
 
     def state_dict(self) -> dict:
         return {f.name: getattr(self.state, f.name) for f in dataclasses.fields(self.state) if f.name != "W_warm"}
