@@ -23,10 +23,10 @@ fl = attn_flops(rp.cpu().numpy(), ci.cpu().numpy(), L.N, L.block, L.head_dim)
 o, lse = P.block_sparse_attn_fwd(q, k, v, rp, ci)
 torch.cuda.synchronize()
 import threading, pynvml
-pynvml.nvmlInit(); hnd = pynvml.nvmlDeviceGetHandleByIndex(0); clk = []; stop = threading.Event()
+pynvml.nvmlInit(); hnd = pynvml.nvmlDeviceGetHandleByIndex(0); clk = []; pw = []; stop = threading.Event()
 def samp():
     while not stop.is_set():
-        clk.append(pynvml.nvmlDeviceGetClockInfo(hnd, pynvml.NVML_CLOCK_SM)); stop.wait(0.01)
+        clk.append(pynvml.nvmlDeviceGetClockInfo(hnd, pynvml.NVML_CLOCK_SM)); pw.append(pynvml.nvmlDeviceGetPowerUsage(hnd) / 1000.0); stop.wait(0.01)
 th = threading.Thread(target=samp); th.start()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
@@ -39,4 +39,4 @@ mhz = float(np.median(clk)) if clk else float("nan")
 nnz = float(masks.sum()); iters_per_sm = nnz / 148
 print(json.dumps({"lib": os.environ.get("MODDIT_LIB_OVERRIDE", "default"), "dbg": os.environ.get("MOD_ATTN_DEBUG", "0"),
                   "density": round(float(masks.mean()), 4), "ms": round(ms, 3), "tflops": round(fl / ms / 1e9, 1),
-                  "sm_mhz": mhz, "cycles_per_block_iter": round(ms * 1e-3 * mhz * 1e6 / iters_per_sm, 1)}))
+                  "sm_mhz": mhz, "watts": round(float(np.median(pw[len(pw)//3:])), 0) if pw else None, "mhz_late": float(np.median(clk[len(clk)//3:])) if clk else None, "cycles_per_block_iter": round(ms * 1e-3 * mhz * 1e6 / iters_per_sm, 1)}))

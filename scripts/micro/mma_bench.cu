@@ -4,27 +4,52 @@
 #include <cstdint>
 #include "../../paper_2601_11641_b200/csrc/sm100.cuh"
 using namespace sm100;
-template <int N, bool TS>
+template <int N, bool TS, int MODE = 0>   // MODE 0: B K-major; 1: B MN-major (like V); 2: S(SS,K-major) + PV(TS,MN-major) alternating;
+// 3: 8 MMAs + commit; 4: 8 MMAs + commit + wait on a completed barrier; 5: 8 MMAs + wait (no commit)
 __global__ void __launch_bounds__(128, 1) k(long long* cyc, int niter) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ uint32_t slot;
-  __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(8) uint64_t bar, bar_a, bar_b;
   for (int i = threadIdx.x; i < 160 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0;
   fence_async_shared();
   if (threadIdx.x < 32) tmem_alloc<512>(&slot);
-  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_mbar_init(); }
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); mbar_init(&bar_a, 1); mbar_init(&bar_b, 1); fence_mbar_init(); mbar_arrive(&bar_b); }
   tc_fence_before(); __syncthreads(); tc_fence_after();
   const uint32_t tmem = slot;
   if (threadIdx.x == 0) {
-    constexpr uint32_t idesc = idesc_bf16_f32(128, N, false, false);
+    constexpr uint32_t idesc = idesc_bf16_f32(128, N, false, MODE == 1);
+    constexpr uint32_t idesc_mn = idesc_bf16_f32(128, N, false, true);
     const uint32_t sa = smem_u32(smem), sb = smem_u32(smem + 32768);  // B: up to 256 rows x 2 atoms = 64KB
     long long t0 = clock64();
     for (int it = 0; it < niter; ++it) {
+      if (MODE == 2) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint64_t ad = smem_desc_sw128(sa + (kk / 4) * 16384 + (kk % 4) * 32, 16, 1024);
+          const uint64_t bd = smem_desc_sw128(sb + (kk / 4) * (N * 128) + (kk % 4) * 32, 16, 1024);
+          mma_ss(tmem, ad, bd, idesc, 1u);
+        }
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint64_t bd = smem_desc_sw128(sb + kk * 2048, 128 * 128, 1024);
+          mma_ts(tmem + 256, tmem + 128 + kk * 8, bd, idesc_mn, 1u);
+        }
+        continue;
+      }
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
-        const uint64_t bd = smem_desc_sw128(sb + (kk / 4) * (N * 128) + (kk % 4) * 32, 16, 1024);
+        const uint64_t bd = MODE == 1 ? smem_desc_sw128(sb + kk * 2048, 128 * 128, 1024)
+                                      : smem_desc_sw128(sb + (kk / 4) * (N * 128) + (kk % 4) * 32, 16, 1024);
         if (TS) mma_ts(tmem, tmem + 384 + kk * 8, bd, idesc, 1u);
+        else if (MODE >= 3) {
+          const uint64_t ad = smem_desc_sw128(sa + (kk / 4) * 16384 + (kk % 4) * 32, 16, 1024);
+          mma_ss(tmem, ad, bd, idesc, 1u);
+          if (kk == 7) {
+            if (MODE == 3 || MODE == 4) mma_commit(&bar_a);
+            if (MODE == 4 || MODE == 5) mbar_wait(&bar_b, 0);
+          }
+        }
         else {
           const uint64_t ad = smem_desc_sw128(sa + (kk / 4) * 16384 + (kk % 4) * 32, 16, 1024);
           mma_ss(tmem, ad, bd, idesc, 1u);
@@ -39,11 +64,11 @@ __global__ void __launch_bounds__(128, 1) k(long long* cyc, int niter) {
   tc_fence_before(); __syncthreads();
   if (threadIdx.x < 32) { tc_fence_after(); tmem_dealloc<512>(tmem); }
 }
-template <int N, bool TS> void run(const char* name) {
+template <int N, bool TS, int MODE = 0> void run(const char* name) {
   long long* d = nullptr;
   cudaError_t e = cudaMalloc(&d, 148 * 8);
   printf("malloc %s\n", cudaGetErrorString(e)); fflush(stdout);
-  auto kern = k<N, TS>;
+  auto kern = k<N, TS, MODE>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024 + 1024);
   int niter = 2000;
   kern<<<148, 128, 160 * 1024 + 1024>>>(d, niter);
@@ -53,7 +78,7 @@ template <int N, bool TS> void run(const char* name) {
   float ms; cudaEventElapsedTime(&ms, e0, e1);
   long long h[148]; cudaMemcpy(h, d, 148 * 8, cudaMemcpyDeviceToHost);
   double avg = 0; for (int i = 0; i < 148; ++i) avg += h[i]; avg /= 148;
-  double flops = 148.0 * niter * 8 * 2.0 * 128 * N * 16;
+  double flops = (MODE == 2 ? 2 : 1) * 148.0 * niter * 8 * 2.0 * 128 * N * 16;
   printf("%-14s %s cycles/MMA=%.1f  ideal=%d  TFLOPS=%.0f  (%.3f ms) err=%s\n", name, TS ? "TS" : "SS", avg / (niter * 8.0),
          128 * N / 256, flops / ms / 1e9, ms, cudaGetErrorString(cudaGetLastError()));
 }
@@ -63,5 +88,11 @@ int main() {
   run<64, false>("M128 N64 K16");
   run<128, true>("M128 N128 K16");
   run<256, true>("M128 N256 K16");
+  run<128, false, 1>("N128 B-MN");
+  run<128, true, 1>("N128 B-MN");
+  run<128, false, 2>("S+PV pair/2");
+  run<128, false, 3>("8+commit");
+  run<128, false, 4>("8+commit+wait");
+  run<128, false, 5>("8+wait");
   return 0;
 }
