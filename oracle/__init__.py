@@ -26,3 +26,4 @@ from .predict import (keep_frames, extrapolate, pattern_keys, select_patterns, b
 from .attention import masked_attention, masked_attention_rows, dense_attention  # noqa: F401
 from .update import reconstruct_history, update_online_mask  # noqa: F401
 from .schedule import OracleSchedule  # noqa: F401
+from .analysis import rel_frobenius, der, reconstruction_nre, linearity_nre  # noqa: F401
