@@ -168,6 +168,28 @@ mod_status mod_collect_exact_sparsity(mod_plan plan, const void* q, const void* 
                                       const int32_t* row_ptr, const int32_t* col_idx, float eta, float* stats,
                                       void* ws, void* stream);
 
+/* ---- analysis metrics (the paper's ablations on its own maps, App. A) ---------- */
+
+/* Relative Frobenius distance per head:  out[b,h] = ||A_bh - B_bh||_F / ||B_bh||_F,  fp64 accumulation
+ * in a fixed order (deterministic).  It is
+ *   DER(t) = ||S^(t) - S^(12)|| / ||S^(12)||        (difference error ratio), and
+ *   NRE(t) = ||S_hat^(t) - S_GT^(t)|| / ||S_GT^(t)||   (normalised reconstruction error),
+ * with the matrix 2-norm read as Frobenius (reading Z20).  a, b: fp32 [B,H,n,n] (device); out: fp64
+ * [B,H] (device).  ||B_bh|| = 0 gives out = 0 when A_bh = B_bh and +inf otherwise.  ws: the plan's
+ * workspace (mod_plan_workspace_bytes). */
+mod_status mod_map_rel_error(mod_plan plan, const float* a, const float* b, double* out, void* ws, void* stream);
+
+/* Linearity NRE of the C/D intensity trajectories (App. A) over one prediction window:
+ *   x_hat_k^(t) = x_curr_k + (x_curr_k - x_prev_k)/(t_curr - t_prev) * (t - t_curr)   (Eq. 6/7),
+ *   out[b,h,k]  = sqrt( (1/S) sum_s (x_k^(t_s) - x_hat_k^(t_s))^2 ) / (max_s x_k^(t_s) - min_s x_k^(t_s))
+ * for the 3n-1 C and D patterns k (frame intensities are not predicted).  x_prev, x_curr: fp64
+ * [B,H,p] anchors at steps t_prev != t_curr; x_traj: fp64 [S,B,H,p] the fitted intensities at the steps
+ * t_steps[0..S-1] (host array); out: fp64 [B,H,3n-1] (device).  A pattern whose S values are all
+ * equal gets NaN (its range is 0).  S >= 1. */
+mod_status mod_linearity_nre(mod_plan plan, const double* x_prev, const double* x_curr, int32_t t_prev,
+                             int32_t t_curr, const double* x_traj, const int32_t* t_steps /*host*/, int32_t S,
+                             double* out, void* stream);
+
 /* Dense mask helper (the warm-up's full attention, Alg. 1): all-ones CSR. */
 mod_status mod_fill_dense_mask(mod_plan plan, int32_t* row_ptr, int32_t* col_idx, void* stream);
 

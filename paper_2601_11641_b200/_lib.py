@@ -63,6 +63,8 @@ SIGNATURES = {
     "mod_block_sparse_attn_fwd": (I32, [P, P, P, P, P, P, P, P, P, P]),
     "mod_fill_dense_mask": (I32, [P, P, P, P]),
     "mod_collect_exact_sparsity": (I32, [P, P, P, P, P, P, C.c_float, P, P, P]),
+    "mod_map_rel_error": (I32, [P, P, P, P, P, P]),
+    "mod_linearity_nre": (I32, [P, P, P, I32, I32, P, C.POINTER(I32), I32, P, P]),
     "mod_last_launch_count": (I32, []),
 }
 

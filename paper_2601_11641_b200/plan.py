@@ -80,7 +80,7 @@ class Plan:
     # ------------------------------------------------------------------ plumbing
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and lib is not None:   # module globals may already be torn down at interpreter exit
             lib.mod_plan_destroy(h)
             self._h = None
 
@@ -173,6 +173,31 @@ class Plan:
         out = self.empty_stats().fill_(float("nan")) if out is None else out
         check(lib.mod_collect_exact_sparsity(self._h, _ptr(q), _ptr(k), _ptr(lse), _ptr(row_ptr), _ptr(col_idx),
                                              eta, _ptr(out), _ptr(self.workspace()), _stream()))
+        return out
+
+    # ------------------------------------------------------------------ analysis metrics (f3)
+    def map_rel_error(self, a, b, out=None):
+        """||a - b||_F / ||b||_F per head (DER; reconstruction NRE) -> fp64 [B, H]."""
+        for t in (a, b):
+            if t.dtype != torch.float32 or tuple(t.shape) != (self.spec.batch, self.spec.heads, self.n, self.n) \
+                    or not t.is_contiguous():
+                raise ValueError(f"maps must be contiguous fp32 {[self.spec.batch, self.spec.heads, self.n, self.n]}")
+        out = torch.empty((self.spec.batch, self.spec.heads), dtype=torch.float64, device=self._dev()) \
+            if out is None else out
+        check(lib.mod_map_rel_error(self._h, _ptr(a), _ptr(b), _ptr(out), _ptr(self.workspace()), _stream()))
+        return out
+
+    def linearity_nre(self, x_prev, x_curr, t_prev: int, t_curr: int, x_traj, t_steps):
+        """App. A linearity NRE of the C/D intensities over the steps ``t_steps`` -> fp64
+        [B, H, 3n-1]; ``x_traj`` is fp64 [S, B, H, p] (the fits at those steps)."""
+        S = len(t_steps)
+        if tuple(x_traj.shape) != (S, self.spec.batch, self.spec.heads, self.p) or x_traj.dtype != torch.float64 \
+                or not x_traj.is_contiguous():
+            raise ValueError(f"x_traj must be contiguous fp64 {[S, self.spec.batch, self.spec.heads, self.p]}")
+        ts = (C.c_int32 * max(S, 1))(*[int(t) for t in t_steps])
+        out = torch.empty((self.spec.batch, self.spec.heads, 3 * self.n - 1), dtype=torch.float64, device=self._dev())
+        check(lib.mod_linearity_nre(self._h, _ptr(x_prev), _ptr(x_curr), t_prev, t_curr, _ptr(x_traj), ts, S,
+                                    _ptr(out), _stream()))
         return out
 
     def dense_mask(self, out=None):
