@@ -271,7 +271,7 @@ def run_ours(args):
             ev["attn"].append((e[1], e[2]))
             ev["rest"].append((e[0], e[1], e[2], e[3]))
 
-    launches_per_step = 3 + 1 + (1 if exact else 2) + 6   # predict (3) + attn + statistic + update (6)
+    launches_per_step = 3 + 1 + (1 if exact else 3) + 6   # predict (3) + attn + statistic (pool, score, norm) + update (6)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()

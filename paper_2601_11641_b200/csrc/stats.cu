@@ -7,14 +7,17 @@
 //   z_ij   = s * qbar_i . kbar_j                                      (s = 1/sqrt(D))
 //   W_ij   = |I_j| e^{z_ij} / sum_j' |I_j'| e^{z_ij'}                 (block mass; ragged blocks Z16)
 //
-// Two kernels:
+// Three kernels:
 //   pool_kernel   -- HBM-bound: streams Q and K once (2*B*H*N*D*2 bytes) with 128-bit
 //                    non-allocating loads; one CTA per (tensor, head, block); fixed-order
 //                    reduction (deterministic).
-//   score_kernel  -- z = qbar kbar^T (n x n x D per head, packed fp32 FFMA2, 4x4 register tiles over
-//                    shared-memory tiles) fused with the log-size bias and the row softmax; one CTA
-//                    owns 64 full rows so the softmax needs no inter-CTA communication.
+//   score_tc_kernel -- z = qbar kbar^T (n x n x D per head) on tcgen05 with a bf16 hi/lo split of the
+//                    fp32 means (3 MMAs per K step), fused with the log-size bias and per-tile row
+//                    (max, sum) partials; softmax_norm_kernel finishes the row softmax.
 #include "common.cuh"
+#include "sm100.cuh"
+
+using namespace sm100;
 
 namespace {
 
@@ -68,145 +71,175 @@ __global__ void __launch_bounds__(256) pool_kernel(const __nv_bfloat16* __restri
   }
 }
 
-// z = s * qbar kbar^T for 64 rows x all n columns of one head per CTA (256 threads, 4 x 4 outputs
-// each, packed FFMA2), fused with ln|I_j| and the row softmax.  The qbar tile is staged once
-// (transposed, D x 64); kbar tiles of 64 columns are prefetched into registers while the previous
-// tile is consumed.
-constexpr int SR = 64, SC = 64;
+// z = s * qbar kbar^T on the tensor cores (north_star: "tensor cores are used ... in the QK^T of the
+// pooled scores"), fused with the log-size bias; the row softmax is split in two passes so that the
+// grid covers every (128-row, 64-column) tile of every head (2 CTAs per SM):
+//   score_tc_kernel  builds the bf16 (hi, lo) split of the fp32 means, hi = bf16(x), lo = bf16(x - hi),
+//                    K-major in the 128B-swizzled layout, one thread issues
+//                    Z = A_hi B_hi^T + A_hi B_lo^T + A_lo B_hi^T (fp32 accumulate in TMEM; the dropped
+//                    lo*lo term is < 2^-16 relative, far inside the 1e-3 bar on W), then thread = row:
+//                    logits v = (s z + ln|I_j|) log2 e -> W, and the tile's (max, sum 2^(v-max)) per row
+//   softmax_norm_kernel  one warp per row: combine the row's tile partials in a fixed order, then
+//                    W = 2^(v - m) / l over the row, coalesced (the logits are L2-resident)
+template <int D>
+struct ScoreCfg {
+  static constexpr int TM = 128, TN = 64;                  // tile rows (MMA M) / columns (MMA N)
+  static constexpr int NATOM = D / 64;
+  static constexpr int A_ATOM = TM * 128, B_ATOM = TN * 128;
+  static constexpr int A_BYTES = A_ATOM * NATOM, B_BYTES = B_ATOM * NATOM;
+  static constexpr int OFF_AH = 0, OFF_AL = A_BYTES, OFF_BH = 2 * A_BYTES, OFF_BL = 2 * A_BYTES + B_BYTES;
+  static constexpr int OFF_BAR = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int SMEM = OFF_BAR + 64 + 1024;          // + alignment slack
+  static constexpr uint32_t IDESC = idesc_bf16_f32(TM, TN, false, false);
+};
 
-__device__ __forceinline__ float2 ffma2s(float2 a, float2 b, float2 c) {
-  float2 d;
-  asm("{.reg .b64 ra, rb, rc, rd;\n mov.b64 ra, {%2,%3};\n mov.b64 rb, {%4,%5};\n mov.b64 rc, {%6,%7};\n"
-      " fma.rn.f32x2 rd, ra, rb, rc;\n mov.b64 {%0,%1}, rd;}"
-      : "=f"(d.x), "=f"(d.y)
-      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
-  return d;
+// ROWS rows from row0 of a [n, D] fp32 matrix -> bf16 hi / lo tiles (K-major, 128B swizzle).
+// 128 threads; thread t handles 16-byte chunks t, t+128, ... (consecutive threads: consecutive
+// chunks of a row -> coalesced loads); batches of 8 chunks keep 16 independent loads in flight.
+template <int D, int ROWS>
+__device__ __forceinline__ void build_split(const float* __restrict__ src, int row0, int n, unsigned char* hi_tile,
+                                            unsigned char* lo_tile, int atom_bytes, int t) {
+  constexpr int CPR = D / 8;                  // 16-byte (8-element) chunks per row
+  constexpr int PER = ROWS * CPR / 128;       // chunks per thread
+  constexpr int BATCH = PER < 8 ? PER : 8;
+#pragma unroll
+  for (int b0 = 0; b0 < PER; b0 += BATCH) {
+    float4 va[BATCH], vb[BATCH];
+#pragma unroll
+    for (int u = 0; u < BATCH; ++u) {
+      const int e = t + (b0 + u) * 128;
+      const int r = e / CPR, k16 = e % CPR;
+      const bool ok = row0 + r < n;
+      const float4* p = reinterpret_cast<const float4*>(src + (size_t)(row0 + r) * D + k16 * 8);
+      va[u] = ok ? __ldg(p) : make_float4(0.f, 0.f, 0.f, 0.f);
+      vb[u] = ok ? __ldg(p + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < BATCH; ++u) {
+      const int e = t + (b0 + u) * 128;
+      const int r = e / CPR, k16 = e % CPR;
+      const float x[8] = {va[u].x, va[u].y, va[u].z, va[u].w, vb[u].x, vb[u].y, vb[u].z, vb[u].w};
+      uint32_t h[4], l[4];
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const __nv_bfloat16 h0 = __float2bfloat16_rn(x[2 * w]), h1 = __float2bfloat16_rn(x[2 * w + 1]);
+        const __nv_bfloat16 l0 = __float2bfloat16_rn(x[2 * w] - __bfloat162float(h0));
+        const __nv_bfloat16 l1 = __float2bfloat16_rn(x[2 * w + 1] - __bfloat162float(h1));
+        h[w] = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
+        l[w] = (uint32_t)__bfloat16_as_ushort(l0) | ((uint32_t)__bfloat16_as_ushort(l1) << 16);
+      }
+      const int off = (k16 >> 3) * atom_bytes + r * 128 + (((k16 & 7) ^ (r & 7)) << 4);
+      *reinterpret_cast<uint4*>(hi_tile + off) = make_uint4(h[0], h[1], h[2], h[3]);
+      *reinterpret_cast<uint4*>(lo_tile + off) = make_uint4(l[0], l[1], l[2], l[3]);
+    }
+  }
 }
 
 template <int D>
-__global__ void __launch_bounds__(256) score_kernel(const float* __restrict__ qbar, const float* __restrict__ kbar,
-                                                     const float* __restrict__ log_sizes, float* __restrict__ W,
-                                                     int n, float scale) {
-  extern __shared__ __align__(16) float sm[];
-  float (*As)[SR + 4] = reinterpret_cast<float(*)[SR + 4]>(sm);                       // [D][SR+4]
-  float (*Bs)[SC + 4] = reinterpret_cast<float(*)[SC + 4]>(sm + D * (SR + 4));        // [D][SC+4]
-  __shared__ float rowmax_s[SR], rowsum_s[SR];
-  const size_t bh = blockIdx.y;
-  const int r0 = blockIdx.x * SR;
+__global__ void __launch_bounds__(128, 2) score_tc_kernel(const float* __restrict__ qbar, const float* __restrict__ kbar,
+                                                          const float* __restrict__ log_sizes, float* __restrict__ W,
+                                                          float2* __restrict__ part, int n, float scale) {
+  using C = ScoreCfg<D>;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* done = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_BAR + 8);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int c0 = blockIdx.x * C::TN, r0 = blockIdx.y * C::TM;
+  const int Tc = gridDim.x;
+  const size_t bh = blockIdx.z;
   const float* Q = qbar + bh * (size_t)n * D;
   const float* K = kbar + bh * (size_t)n * D;
   float* Wh = W + bh * (size_t)n * n;
-  const int t = threadIdx.x;
-  const int tr = (t / 16) * 4;       // rows tr..tr+3 of the tile
-  const int tc = (t % 16) * 4;       // cols tc..tc+3 of the tile
-  const float scale_l2 = scale * 1.4426950408889634f;
-  constexpr int V4 = SR * D / 4 / 256;   // float4 loads per thread per tile
-  // stage qbar (transposed)
-#pragma unroll
-  for (int u = 0; u < V4; ++u) {
-    const int e = t + u * 256;            // float4 index: consecutive threads -> consecutive rows
-    const int r = e % SR, d4 = (e / SR) * 4; // (transposed shared-memory stores stay conflict-free)
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (r0 + r < n) v = *reinterpret_cast<const float4*>(Q + (size_t)(r0 + r) * D + d4);
-    As[d4][r] = v.x; As[d4 + 1][r] = v.y; As[d4 + 2][r] = v.z; As[d4 + 3][r] = v.w;
+  const float L2E = 1.4426950408889634f;
+
+  if (threadIdx.x == 0) {
+    mbar_init(done, 1);
+    fence_mbar_init();
   }
-  float4 pre[V4];
-  auto load_b = [&](int c0) {
-#pragma unroll
-    for (int u = 0; u < V4; ++u) {
-      const int e = t + u * 256;
-      const int c = e % SC, d4 = (e / SC) * 4;
-      pre[u] = (c0 + c < n) ? *reinterpret_cast<const float4*>(K + (size_t)(c0 + c) * D + d4)
-                            : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-  };
-  float m_run[4], l_run[4];
-#pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    m_run[a] = -INFINITY;
-    l_run[a] = 0.f;
-  }
-  load_b(0);
-  for (int c0 = 0; c0 < n; c0 += SC) {
-    __syncthreads();                      // previous tile consumed
-#pragma unroll
-    for (int u = 0; u < V4; ++u) {
-      const int e = t + u * 256;
-      const int c = e % SC, d4 = (e / SC) * 4;
-      Bs[d4][c] = pre[u].x; Bs[d4 + 1][c] = pre[u].y; Bs[d4 + 2][c] = pre[u].z; Bs[d4 + 3][c] = pre[u].w;
-    }
-    __syncthreads();
-    if (c0 + SC < n) load_b(c0 + SC);     // prefetch the next tile while computing this one
-    float2 acc[4][2];
-#pragma unroll
-    for (int x = 0; x < 4; ++x) acc[x][0] = acc[x][1] = make_float2(0.f, 0.f);
-    // software-pipelined: the shared-memory operands of step d+1 are loaded before step d's FFMA2s
-    float4 an = *reinterpret_cast<const float4*>(&As[0][tr]);
-    float4 bn = *reinterpret_cast<const float4*>(&Bs[0][tc]);
-#pragma unroll 4
-    for (int d = 0; d < D; ++d) {
-      const float4 a = an, b = bn;
-      if (d + 1 < D) {
-        an = *reinterpret_cast<const float4*>(&As[d + 1][tr]);
-        bn = *reinterpret_cast<const float4*>(&Bs[d + 1][tc]);
-      }
-      const float av[4] = {a.x, a.y, a.z, a.w};
-      const float2 b01 = make_float2(b.x, b.y), b23 = make_float2(b.z, b.w);
-#pragma unroll
-      for (int x = 0; x < 4; ++x) {
-        acc[x][0] = ffma2s(make_float2(av[x], av[x]), b01, acc[x][0]);
-        acc[x][1] = ffma2s(make_float2(av[x], av[x]), b23, acc[x][1]);
-      }
-    }
-    // logits = s*z + ln|I_j|, written in place; online row max / sum
-#pragma unroll
-    for (int x = 0; x < 4; ++x) {
-      const int r = r0 + tr + x;
-      const float zz[4] = {acc[x][0].x, acc[x][0].y, acc[x][1].x, acc[x][1].y};
-      float v[4];
-#pragma unroll
-      for (int y = 0; y < 4; ++y) {   // log2-domain logits: (s z + ln|I_j|) * log2(e)
-        const int c = c0 + tc + y;
-        v[y] = (c < n) ? fmaf(zz[y], scale_l2, log_sizes[c] * 1.4426950408889634f) : -INFINITY;
-        if (r < n && c < n) Wh[(size_t)r * n + c] = v[y];
-      }
-      const float mx = fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3]));
-      const float mnew = fmaxf(m_run[x], mx);
-      if (mnew > -INFINITY) {
-        float sacc = l_run[x] * exp2f(m_run[x] - mnew);
-#pragma unroll
-        for (int y = 0; y < 4; ++y) sacc += exp2f(v[y] - mnew);
-        l_run[x] = sacc;
-        m_run[x] = mnew;
-      }
-    }
-  }
-  // combine the 16 column-threads of each row (16 consecutive lanes)
-#pragma unroll
-  for (int x = 0; x < 4; ++x) {
-    float m = m_run[x];
-#pragma unroll
-    for (int o = 8; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    float l = (m_run[x] > -INFINITY) ? l_run[x] * exp2f(m_run[x] - m) : 0.f;
-#pragma unroll
-    for (int o = 8; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
-    if ((t % 16) == 0) {
-      rowmax_s[tr + x] = m;
-      rowsum_s[tr + x] = l;
-    }
-  }
+  if (warp == 0) tmem_alloc<64>(tmem_slot);
+  build_split<D, C::TM>(Q, r0, n, smem + C::OFF_AH, smem + C::OFF_AL, C::A_ATOM, threadIdx.x);
+  build_split<D, C::TN>(K, c0, n, smem + C::OFF_BH, smem + C::OFF_BL, C::B_ATOM, threadIdx.x);
+  fence_async_shared();
+  tc_fence_before();
   __syncthreads();
-  // W = exp(logit - m) / l, in place (this CTA owns rows r0..r0+63)
-  for (int rr = t / 32; rr < SR; rr += 8) {
-    const int r = r0 + rr;
-    if (r >= n) break;
-    const float m = rowmax_s[rr];
-    const float invl = 1.0f / rowsum_s[rr];
-    for (int c = t % 32; c < n; c += 32) {
-      float* p = &Wh[(size_t)r * n + c];
-      *p = exp2f(*p - m) * invl;
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) {
+    const uint32_t ah = smem_u32(smem + C::OFF_AH), al = smem_u32(smem + C::OFF_AL);
+    const uint32_t bhs = smem_u32(smem + C::OFF_BH), bls = smem_u32(smem + C::OFF_BL);
+#pragma unroll
+    for (int kk = 0; kk < D / 16; ++kk) {
+      const uint32_t ko = (kk % 4) * 32;
+      const uint64_t dah = smem_desc_sw128(ah + (kk / 4) * C::A_ATOM + ko, 16, 1024);
+      const uint64_t dal = smem_desc_sw128(al + (kk / 4) * C::A_ATOM + ko, 16, 1024);
+      const uint64_t dbh = smem_desc_sw128(bhs + (kk / 4) * C::B_ATOM + ko, 16, 1024);
+      const uint64_t dbl = smem_desc_sw128(bls + (kk / 4) * C::B_ATOM + ko, 16, 1024);
+      mma_ss(tmem, dah, dbh, C::IDESC, kk > 0 ? 1u : 0u);
+      mma_ss(tmem, dah, dbl, C::IDESC, 1u);
+      mma_ss(tmem, dal, dbh, C::IDESC, 1u);
+    }
+    mma_commit(done);
+  }
+  // epilogue: thread = tile row (warp w reads TMEM lane quarter w)
+  const int row = warp * 32 + lane;
+  const int gr = r0 + row;
+  mbar_wait(done, 0);
+  tc_fence_after();
+  uint32_t z[64];
+  tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16), *reinterpret_cast<uint32_t(*)[32]>(&z[0]));
+  tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + 32, *reinterpret_cast<uint32_t(*)[32]>(&z[32]));
+  tmem_ld_wait();
+  const int valid = min(C::TN, n - c0);
+  const float scale_l2 = scale * L2E;
+  float mx = -INFINITY;
+#pragma unroll
+  for (int e = 0; e < 64; ++e) {
+    const float v = e < valid ? fmaf(__uint_as_float(z[e]), scale_l2, __ldg(log_sizes + c0 + e) * L2E) : -INFINITY;
+    z[e] = __float_as_uint(v);
+    mx = fmaxf(mx, v);
+  }
+  float sum = 0.f;
+#pragma unroll
+  for (int e = 0; e < 64; ++e) sum += exp2f(__uint_as_float(z[e]) - mx);
+  if (gr < n) {
+    part[(bh * n + gr) * Tc + blockIdx.x] = make_float2(mx, sum);
+    float* dst = Wh + (size_t)gr * n + c0;
+    if (valid == 64 && (((uintptr_t)dst & 15) == 0)) {
+#pragma unroll
+      for (int e = 0; e < 16; ++e)
+        reinterpret_cast<uint4*>(dst)[e] = make_uint4(z[4 * e], z[4 * e + 1], z[4 * e + 2], z[4 * e + 3]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 64; ++e)
+        if (e < valid) dst[e] = __uint_as_float(z[e]);
     }
   }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<64>(tmem);
+  }
+}
+
+// one warp per (head, row): m = max_t m_t, l = sum_t l_t 2^(m_t - m) in tile order, W = 2^(v - m) / l
+__global__ void __launch_bounds__(256) softmax_norm_kernel(float* __restrict__ W, const float2* __restrict__ part,
+                                                           int n, int Tc, size_t rows) {
+  const size_t gw = (size_t)blockIdx.x * 8 + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (gw >= rows) return;
+  const float2 pt = lane < Tc ? part[gw * Tc + lane] : make_float2(-INFINITY, 0.f);
+  float m = pt.x;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  // fixed-order sum over the tiles (lane order), so the result does not depend on scheduling
+  const float term = (lane < Tc && pt.x > -INFINITY) ? pt.y * exp2f(pt.x - m) : 0.f;
+  float l = 0.f;
+  for (int t = 0; t < Tc; ++t) l += __shfl_sync(0xffffffffu, term, t);
+  const float invl = 1.0f / l;
+  float* p = W + gw * n;
+  for (int c = lane; c < n; c += 32) p[c] = exp2f(p[c] - m) * invl;
 }
 
 }  // namespace
@@ -228,15 +261,22 @@ extern "C" mod_status mod_collect_block_stats(mod_plan P, const void* q, const v
     pool_kernel<64><<<pg, 256, 0, s>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k, qbar, kbar, P->N, n,
                                        P->L.block);
   MOD_LAUNCH_CHECK();
-  const size_t ssm = (size_t)D * ((SR + 4) + (SC + 4)) * sizeof(float);
+  const int Tc = (n + 63) / 64;   // <= 32 column tiles (n <= kMaxBlocks = 2048)
+  const dim3 sg(Tc, (n + 127) / 128, BH);
+  float2* part = reinterpret_cast<float2*>(static_cast<char*>(ws) + P->ws_part);   // [BH, n, Tc] (free during K1)
   if (D == 128) {
-    MOD_CUDA(cudaFuncSetAttribute(score_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
-    score_kernel<128><<<dim3((n + SR - 1) / SR, BH), 256, ssm, s>>>(qbar, kbar, P->d_log_sizes, stats, n, P->scale);
+    MOD_CUDA(cudaFuncSetAttribute(score_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  ScoreCfg<128>::SMEM));
+    score_tc_kernel<128><<<sg, 128, ScoreCfg<128>::SMEM, s>>>(qbar, kbar, P->d_log_sizes, stats, part, n, P->scale);
   } else {
-    MOD_CUDA(cudaFuncSetAttribute(score_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
-    score_kernel<64><<<dim3((n + SR - 1) / SR, BH), 256, ssm, s>>>(qbar, kbar, P->d_log_sizes, stats, n, P->scale);
+    MOD_CUDA(cudaFuncSetAttribute(score_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  ScoreCfg<64>::SMEM));
+    score_tc_kernel<64><<<sg, 128, ScoreCfg<64>::SMEM, s>>>(qbar, kbar, P->d_log_sizes, stats, part, n, P->scale);
   }
   MOD_LAUNCH_CHECK();
-  mod_note_launches(2);
+  const size_t rows = (size_t)BH * n;
+  softmax_norm_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(stats, part, n, Tc, rows);
+  MOD_LAUNCH_CHECK();
+  mod_note_launches(3);
   return MOD_OK;
 }
