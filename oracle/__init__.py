@@ -27,3 +27,5 @@ from .attention import masked_attention, masked_attention_rows, dense_attention 
 from .update import reconstruct_history, update_online_mask  # noqa: F401
 from .schedule import OracleSchedule  # noqa: F401
 from .analysis import rel_frobenius, der, reconstruction_nre, linearity_nre  # noqa: F401
+from .quant import (round_e4m3, quantize_int8_blocks, quantize_e4m3_channels, dequantized_qkv,  # noqa: F401
+                    quantized_attention_rows)
