@@ -168,6 +168,34 @@ mod_status mod_collect_exact_sparsity(mod_plan plan, const void* q, const void* 
                                       const int32_t* row_ptr, const int32_t* col_idx, float eta, float* stats,
                                       void* ws, void* stream);
 
+/* ---- quantized sparse attention ------------------------------------------------
+ * The paper's sparse stage is SageAttention, whose precision PAPER.md does not state.
+ * Reading Z30 fixes a Sage-style scheme: Q and K symmetric INT8 per (head, 128-token
+ * block), s = absmax/127, code = rint(x * (127/absmax)) in fp32; V FP8 e4m3 per (head, channel),
+ * s_d = absmax_d/448, code = RN_e4m3(v * (448/absmax_d)) in fp32 (saturating); the attention takes
+ * S = s_q s_k (Q8 K8^T) on the INT8 tensor cores, P rounded to e4m3, O = (P V8) s_d on the FP8
+ * tensor cores, fp32 softmax and accumulation.  Head dim 128 and block 128 only
+ * (MOD_ERR_UNSUPPORTED otherwise).
+ *
+ * Quantized operand buffer (device, caller-allocated, mod_quant_buffer_bytes), byte offsets from
+ * mod_quant_buffer_layout (6 entries, in this order):
+ *   [0] q8   int8  [B,H,N,D]        [1] k8  int8  [B,H,N,D]
+ *   [2] vt8  e4m3  [B,H,D,Np]  V transposed (token-contiguous), Np = N rounded up to 16; tokens in
+ *                              [N, Np) are zero
+ *   [3] q_scale fp32 [B,H,n]   [4] k_scale fp32 [B,H,n]   [5] v_scale fp32 [B,H,D]
+ * (the buffer also holds a [B,H,D] uint32 scratch for the V channel maxima after [5]). */
+size_t mod_quant_buffer_bytes(mod_plan plan);
+mod_status mod_quant_buffer_layout(mod_plan plan, size_t* offsets /*host, 6 entries*/);
+
+/* Quantize bf16 Q, K, V [B,H,N,D] into qbuf (3 launches + 1 memset: V channel maxima, Q/K blocks,
+ * V transpose).  Deterministic. */
+mod_status mod_quantize_qkv(mod_plan plan, const void* q, const void* k, const void* v, void* qbuf, void* stream);
+
+/* K4 on the quantized operands: same index lists and outputs as mod_block_sparse_attn_fwd
+ * (o bf16 [B,H,N,D], lse nullable fp32 [B,H,N]; empty list -> O = 0, lse = -inf). */
+mod_status mod_block_sparse_attn_fwd_q8(mod_plan plan, const void* qbuf, const int32_t* row_ptr,
+                                        const int32_t* col_idx, void* o, float* lse, void* ws, void* stream);
+
 /* ---- analysis metrics (the paper's ablations on its own maps, App. A) ---------- */
 
 /* Relative Frobenius distance per head:  out[b,h] = ||A_bh - B_bh||_F / ||B_bh||_F,  fp64 accumulation

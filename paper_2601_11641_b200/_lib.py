@@ -63,6 +63,10 @@ SIGNATURES = {
     "mod_block_sparse_attn_fwd": (I32, [P, P, P, P, P, P, P, P, P, P]),
     "mod_fill_dense_mask": (I32, [P, P, P, P]),
     "mod_collect_exact_sparsity": (I32, [P, P, P, P, P, P, C.c_float, P, P, P]),
+    "mod_quant_buffer_bytes": (C.c_size_t, [P]),
+    "mod_quant_buffer_layout": (I32, [P, C.POINTER(C.c_size_t)]),
+    "mod_quantize_qkv": (I32, [P, P, P, P, P, P]),
+    "mod_block_sparse_attn_fwd_q8": (I32, [P, P, P, P, P, P, P, P]),
     "mod_map_rel_error": (I32, [P, P, P, P, P, P]),
     "mod_linearity_nre": (I32, [P, P, P, I32, I32, P, C.POINTER(I32), I32, P, P]),
     "mod_last_launch_count": (I32, []),

@@ -175,6 +175,46 @@ class Plan:
                                              eta, _ptr(out), _ptr(self.workspace()), _stream()))
         return out
 
+    # ------------------------------------------------------------------ quantized attention (f2)
+    def quant_buffer(self) -> torch.Tensor:
+        """Caller-owned buffer for the quantized operands (layout: include/moddit.h, reading Z30)."""
+        nbytes = lib.mod_quant_buffer_bytes(self._h)
+        if nbytes == 0:
+            check(lib.mod_quant_buffer_layout(self._h, (C.c_size_t * 6)()))   # raises with the reason
+        return torch.empty(nbytes, dtype=torch.uint8, device=self._dev())
+
+    def quant_views(self, qbuf: torch.Tensor) -> dict:
+        """Typed views of a quantized-operand buffer: q8, k8 int8 [B,H,N,D]; vt8 uint8 (e4m3 bits)
+        [B,H,D,Np]; q_scale, k_scale fp32 [B,H,n]; v_scale fp32 [B,H,D]."""
+        off = (C.c_size_t * 6)()
+        check(lib.mod_quant_buffer_layout(self._h, off))
+        B, H, N, D, n = self.spec.batch, self.spec.heads, self.N, self.spec.head_dim, self.n
+        Np = (N + 15) // 16 * 16
+
+        def view(o, count, dtype, shape):
+            return qbuf[o:o + count * torch.tensor([], dtype=dtype).element_size()].view(dtype).view(shape)
+        return {"q8": view(off[0], B * H * N * D, torch.int8, (B, H, N, D)),
+                "k8": view(off[1], B * H * N * D, torch.int8, (B, H, N, D)),
+                "vt8": view(off[2], B * H * D * Np, torch.uint8, (B, H, D, Np)),
+                "q_scale": view(off[3], B * H * n, torch.float32, (B, H, n)),
+                "k_scale": view(off[4], B * H * n, torch.float32, (B, H, n)),
+                "v_scale": view(off[5], B * H * D, torch.float32, (B, H, D))}
+
+    def quantize_qkv(self, q, k, v, out=None) -> torch.Tensor:
+        self._check_qkv(q, k, v)
+        qbuf = self.quant_buffer() if out is None else out
+        check(lib.mod_quantize_qkv(self._h, _ptr(q), _ptr(k), _ptr(v), _ptr(qbuf), _stream()))
+        return qbuf
+
+    def block_sparse_attn_fwd_q8(self, qbuf, row_ptr, col_idx, out=None, lse=None, want_lse: bool = True):
+        B, H, N, D = self.spec.batch, self.spec.heads, self.N, self.spec.head_dim
+        o = torch.empty((B, H, N, D), dtype=torch.bfloat16, device=self._dev()) if out is None else out
+        if lse is None and want_lse:
+            lse = torch.empty((B, H, N), dtype=torch.float32, device=self._dev())
+        check(lib.mod_block_sparse_attn_fwd_q8(self._h, _ptr(qbuf), _ptr(row_ptr), _ptr(col_idx), _ptr(o), _ptr(lse),
+                                               _ptr(self.workspace()), _stream()))
+        return o, lse
+
     # ------------------------------------------------------------------ analysis metrics (f3)
     def map_rel_error(self, a, b, out=None):
         """||a - b||_F / ||b||_F per head (DER; reconstruction NRE) -> fp64 [B, H]."""
