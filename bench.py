@@ -246,6 +246,11 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     ev = {k_: [] for k_ in ("attn", "rest")}
 
+    q8 = args.precision == "q8"
+    if q8 and exact:
+        raise SystemExit("--precision q8 with --stat exact is not supported (the exact statistic needs the bf16 lse)")
+    qbuf = P.quant_buffer() if q8 else None
+
     def step(timed_kernels=False):
         if seq is not None:
             for dst, src in zip((q, k, v), seq):
@@ -256,7 +261,11 @@ def run_ours(args):
         P.predict_block_mask(x_prev0, x_curr0, M_WARMUP - 1, M_WARMUP, t_step, keep, top_k=K, out=(rp, ci))
         if timed_kernels:
             e[1].record(stream)
-        P.block_sparse_attn_fwd(q, k, v, rp, ci, out=o, lse=lse)
+        if q8:   # SURVEY f2 (reading Z30): quantize Q, K, V, then INT8 QK^T / FP8 PV attention
+            P.quantize_qkv(q, k, v, out=qbuf)
+            P.block_sparse_attn_fwd_q8(qbuf, rp, ci, out=o, lse=lse)
+        else:
+            P.block_sparse_attn_fwd(q, k, v, rp, ci, out=o, lse=lse)
         if timed_kernels:
             e[2].record(stream)
         if exact:   # Eq. 2 on the masked map of this step (lse over the kept blocks, reading Z12)
@@ -271,7 +280,7 @@ def run_ours(args):
             ev["attn"].append((e[1], e[2]))
             ev["rest"].append((e[0], e[1], e[2], e[3]))
 
-    launches_per_step = 3 + 1 + (1 if exact else 3) + 6   # predict (3) + attn + statistic (pool, score, norm) + update (6)
+    launches_per_step = 3 + (4 if q8 else 1) + (1 if exact else 3) + 6   # predict (3) + attn (+3 quantize) + statistic (pool, score, norm) + update (6)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -302,7 +311,8 @@ def run_ours(args):
 
     out = {"metric": METRIC, "value": round(value, 2), "unit": "TFLOPS", "n_gpus": ws, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong",
-           "vs_baseline": None, "dtype": "bf16", "data": "synthetic (Family S, seeded; SURVEY 8(d))"}
+           "vs_baseline": None, "dtype": "int8/e4m3 (f32 softmax)" if q8 else "bf16",
+           "data": "synthetic (Family S, seeded; SURVEY 8(d))"}
 
     # ---- dense comparators (rank 0, 1 GPU shape of its heads): library SDPA + our K4 with all-ones CSR
     dense = {}
@@ -353,9 +363,13 @@ def run_ours(args):
             traffic = json.load(open(tp)).get(args.config)
         except Exception:
             traffic = None
-    roof = {"bound": "tensor", "achieved": round(attn_tflops, 1), "peak": burst, "unit": "TFLOP/s",
-            "frac": round(attn_tflops / burst, 4), "frac_of_sustained": round(attn_tflops / sustained, 4),
-            "peak_source": peak_src, "traffic": traffic, "kernel": "attn_fwd_kernel<128,128>",
+    # the quantized kernel's peak: the measured bf16 figure x the guide's nominal 2x ratio for 8-bit MMAs
+    pk = burst * (2 if q8 else 1)
+    roof = {"bound": "tensor", "achieved": round(attn_tflops, 1), "peak": pk, "unit": "TFLOP/s",
+            "frac": round(attn_tflops / pk, 4), "frac_of_sustained": round(attn_tflops / (sustained * (2 if q8 else 1)), 4),
+            "peak_source": peak_src + (" (bf16 x 2, nominal 8-bit ratio)" if q8 else ""),
+            "traffic": None if q8 else traffic,
+            "kernel": "quantize (3 kernels) + attn_q8_kernel" if q8 else "attn_fwd_kernel<128,128>",
             "algorithmic_flops_per_launch": flops_local}
 
     out.update({
@@ -480,6 +494,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-blocks", type=int, default=4)
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "q8"],
+                    help="attention operands: bf16 (headline) or the Sage-style INT8/FP8 path (SURVEY f2)")
     ap.add_argument("--stat", default="pooled", choices=["pooled", "exact"],
                     help="block statistic: pooled (north_star (1)) or the paper's exact Eq. 2 (SURVEY f1)")
     ap.add_argument("--eta", type=float, default=1e-4)

@@ -33,16 +33,21 @@ class ScheduleState:
 class Schedule:
     def __init__(self, plan: Plan, T: int = 50, m: int = 12, dt: int = 10, top_k: int | None = None,
                  select_mode: int | None = None, select_param: float | None = None, stat: str = "pooled",
-                 eta: float = 1e-4):
+                 eta: float = 1e-4, precision: str = "bf16"):
         if not (1 <= m < T) or dt < 1 or m < 2:
             raise ValueError(f"bad schedule T={T} m={m} dt={dt}")
         if stat not in ("pooled", "exact"):
             raise ValueError(f"stat={stat!r} must be 'pooled' or 'exact'")
+        if precision not in ("bf16", "q8"):
+            raise ValueError(f"precision={precision!r} must be 'bf16' or 'q8'")
+        if precision == "q8" and stat == "exact":
+            raise ValueError("precision='q8' needs stat='pooled' (the exact statistic thresholds the bf16 lse)")
         if stat == "exact" and plan.config["masked_renorm"]:
             raise ValueError("stat='exact' needs a Plan with masked_renorm=False: the masked map is already "
                              "renormalised by the sparse attention's lse (reading Z12)")
         self.P, self.T, self.m, self.dt = plan, T, m, dt
-        self.stat, self.eta = stat, eta
+        self.stat, self.eta, self.precision = stat, eta, precision
+        self._qbuf = None
         self.sel = dict(top_k=top_k, select_mode=select_mode, select_param=select_param)
         self.state = ScheduleState()
         self._dense = None
@@ -77,7 +82,13 @@ class Schedule:
             self.last_mask = (rp, ci)
             return o, l
         rp, ci = P.predict_block_mask(S.x_prev, S.x_curr, S.t_prev, S.t_curr, t, S.keep, **self.sel)
-        o, l = P.block_sparse_attn_fwd(q, k, v, rp, ci, out=out, lse=lse)
+        if self.precision == "q8":   # sparse steps on the Sage-style quantized path (reading Z30)
+            if self._qbuf is None:
+                self._qbuf = P.quant_buffer()
+            P.quantize_qkv(q, k, v, out=self._qbuf)
+            o, l = P.block_sparse_attn_fwd_q8(self._qbuf, rp, ci, out=out, lse=lse)
+        else:
+            o, l = P.block_sparse_attn_fwd(q, k, v, rp, ci, out=out, lse=lse)
         if self.is_update_step(t):
             W = self._stat(q, k, l, rp, ci)
             P.update_online_mask(W, rp, ci, S.hist, S.x_prev, S.x_curr)

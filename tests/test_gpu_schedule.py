@@ -57,3 +57,32 @@ def test_schedule_exact_statistic_matches_oracle_tiny():
         err = np.abs(o.double().cpu().numpy() - o_ref)
         assert err.max() <= 2e-2 and err.mean() <= 2e-3
     assert agree >= 27
+
+
+def test_schedule_q8_same_masks_as_bf16():
+    """Alg. 1 with the quantized sparse attention: the pooled statistic does not depend on the
+    attention's precision, so every step's mask is bit-identical to the bf16 schedule's; the outputs
+    agree to the quantization error (DESIGN.md parity bar for f2)."""
+    import paper_2601_11641_b200 as M
+    from paper_2601_11641_b200.schedule import Schedule
+    w = syn.Workload("small-prefix", 1, 3, 128, 40, 3, 20, 19, 128)
+    P = M.Plan(w, top_k=6)
+    a = Schedule(P, T=30, m=12, dt=10)
+    b = Schedule(P, T=30, m=12, dt=10, precision="q8")
+    for t in range(1, 31):
+        q, k, v = syn.family_s(w, step=t, device="cuda")
+        oa, _ = a.step(t, q, k, v)
+        oa = oa.clone()
+        ob, _ = b.step(t, q, k, v)
+        (ra, ca), (rb, cb) = a.last_mask, b.last_mask
+        assert torch.equal(ra, rb)                                          # col_idx: used prefix only
+        for h in range(w.heads):
+            nnz = int(ra[0, h, -1])
+            assert torch.equal(ca[0, h, :nnz], cb[0, h, :nnz])
+        d = (oa.float() - ob.float()).abs()
+        if t <= 12:
+            assert d.max().item() == 0.0                                  # warm-up: same bf16 kernel
+        else:
+            assert d.max().item() <= 0.1 and d.mean().item() <= 6e-3
+    with pytest.raises(ValueError, match="stat='pooled'"):
+        Schedule(P, precision="q8", stat="exact")
