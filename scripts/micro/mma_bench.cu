@@ -5,7 +5,8 @@
 #include "../../paper_2601_11641_b200/csrc/sm100.cuh"
 using namespace sm100;
 template <int N, bool TS, int MODE = 0>   // MODE 0: B K-major; 1: B MN-major (like V); 2: S(SS,K-major) + PV(TS,MN-major) alternating;
-// 3: 8 MMAs + commit; 4: 8 MMAs + commit + wait on a completed barrier; 5: 8 MMAs + wait (no commit)
+// 3: 8 MMAs + commit; 4: 8 MMAs + commit + wait on a completed barrier; 5: 8 MMAs + wait (no commit);
+// 6: SS MMAs while warps 1-3 stream tcgen05.ld/st over other TMEM columns (softmax-like traffic); 7: same with TS MMAs
 __global__ void __launch_bounds__(128, 1) k(long long* cyc, int niter) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -17,6 +18,38 @@ __global__ void __launch_bounds__(128, 1) k(long long* cyc, int niter) {
   if (threadIdx.x == 0) { mbar_init(&bar, 1); mbar_init(&bar_a, 1); mbar_init(&bar_b, 1); fence_mbar_init(); mbar_arrive(&bar_b); }
   tc_fence_before(); __syncthreads(); tc_fence_after();
   const uint32_t tmem = slot;
+  __shared__ volatile int stop_flag;
+  if (threadIdx.x == 0) stop_flag = 0;
+  __syncthreads();
+  if ((MODE == 8 || MODE == 9) && threadIdx.x >= 32) {
+    // warps 1-3: stream 16-byte shared-memory stores over [96 KB, 160 KB) (TMA-write-like traffic)
+    uint4* p = reinterpret_cast<uint4*>(smem + 96 * 1024);
+    const uint4 val = make_uint4(threadIdx.x, 1, 2, 3);
+    int i = threadIdx.x - 32;
+    while (!stop_flag) {
+#pragma unroll 8
+      for (int u = 0; u < 64; ++u) {
+        p[i] = val;
+        i += 96;
+        if (i >= 4096) i -= 4096;
+      }
+    }
+  }
+  if ((MODE == 6 || MODE == 7) && threadIdx.x >= 32) {
+    // warps 1-3: lane quarters 1-3, columns [256, 384): ld 32 columns, st them back, repeat
+    const int w = threadIdx.x / 32;
+    const uint32_t base = tmem + ((uint32_t)(w * 32) << 16) + 256;
+    uint32_t r[32];
+    while (!stop_flag) {
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        tmem_ld32(base + c * 32, r);
+        tmem_ld_wait();
+        tmem_st32(base + c * 32, r);
+      }
+      tmem_st_wait();
+    }
+  }
   if (threadIdx.x == 0) {
     constexpr uint32_t idesc = idesc_bf16_f32(128, N, false, MODE == 1);
     constexpr uint32_t idesc_mn = idesc_bf16_f32(128, N, false, true);
@@ -41,7 +74,7 @@ __global__ void __launch_bounds__(128, 1) k(long long* cyc, int niter) {
       for (int kk = 0; kk < 8; ++kk) {
         const uint64_t bd = MODE == 1 ? smem_desc_sw128(sb + kk * 2048, 128 * 128, 1024)
                                       : smem_desc_sw128(sb + (kk / 4) * (N * 128) + (kk % 4) * 32, 16, 1024);
-        if (TS) mma_ts(tmem, tmem + 384 + kk * 8, bd, idesc, 1u);
+        if (TS || MODE == 7 || MODE == 9) mma_ts(tmem, tmem + 384 + kk * 8, bd, idesc, 1u);
         else if (MODE >= 3) {
           const uint64_t ad = smem_desc_sw128(sa + (kk / 4) * 16384 + (kk % 4) * 32, 16, 1024);
           mma_ss(tmem, ad, bd, idesc, 1u);
@@ -60,6 +93,7 @@ __global__ void __launch_bounds__(128, 1) k(long long* cyc, int niter) {
     mbar_wait(&bar, 0);
     long long t1 = clock64();
     cyc[blockIdx.x] = t1 - t0;
+    stop_flag = 1;
   }
   tc_fence_before(); __syncthreads();
   if (threadIdx.x < 32) { tc_fence_after(); tmem_dealloc<512>(tmem); }
@@ -94,5 +128,9 @@ int main() {
   run<128, false, 3>("8+commit");
   run<128, false, 4>("8+commit+wait");
   run<128, false, 5>("8+wait");
+  run<128, false, 6>("SS + TMEM ld/st");
+  run<128, false, 7>("TS + TMEM ld/st");
+  run<128, false, 8>("SS + smem stores");
+  run<128, false, 9>("TS + smem stores");
   return 0;
 }
