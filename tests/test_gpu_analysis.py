@@ -107,3 +107,16 @@ def test_reconstruction_nre_of_the_gpu_update(M):
         want = O.reconstruction_nre(ref[0, h], gt.double().cpu().numpy()[0, h])
         assert nre[0, h] == pytest.approx(want, rel=1e-12)
         assert 0 < nre[0, h] < math.inf
+
+
+def test_map_rel_error_full_size(M):
+    """Hunyuan 720p maps (n = 929, 24 heads) in the launch configuration the analysis script times."""
+    w = syn.HUNYUAN
+    L = olayout(w)
+    P = M.Plan(w)
+    A = syn.random_stats(w.batch, w.heads, L.n, seed=71, device="cuda")
+    B = syn.random_stats(w.batch, w.heads, L.n, seed=72, device="cuda")
+    out = P.map_rel_error(A, B).cpu().numpy()
+    An, Bn = A.cpu().numpy(), B.cpu().numpy()
+    for h in (0, 11, w.heads - 1):
+        assert out[0, h] == pytest.approx(O.rel_frobenius(An[0, h], Bn[0, h]), rel=1e-12)

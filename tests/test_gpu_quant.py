@@ -109,3 +109,38 @@ def test_quant_unsupported_layouts(M):
     assert M.lib.mod_quant_buffer_bytes(P.handle) == 0
     with pytest.raises(M.ModditError, match="head_dim=128, block=128"):
         P.quant_buffer()
+
+
+@pytest.mark.parametrize("w", [syn.HUNYUAN, syn.WAN], ids=lambda w: w.name)
+def test_attention_q8_full_size_sampled(M, w):
+    """Full BASELINE shapes (D = 128), structured masks; codes of the sampled heads bit-exact, O of
+    sampled query blocks (first, last ragged, heaviest row, random) within the f2 bar."""
+    L = olayout(w)
+    P = M.Plan(w)
+    q, k, v = syn.family_s(w, step=7, device="cuda")
+    rng = np.random.default_rng(81)
+    masks = np.zeros((1, w.heads, L.n, L.n), dtype=bool)
+    for h in range(w.heads):
+        sel = O.select_patterns(rng.standard_normal(3 * L.n - 1), L.n, O.SELECT_TOPK, max(4, L.n // 10))
+        masks[0, h] = O.block_mask(sel, rng.random(L.frames) < 0.7, L, True)
+    rp, ci = masks_to_csr(masks)
+    qb = P.quantize_qkv(q, k, v)
+    o, lse = P.block_sparse_attn_fwd_q8(qb, rp, ci)
+    torch.cuda.synchronize()
+    views = P.quant_views(qb)
+    errs = []
+    for h in (0, w.heads - 1):
+        Qh, Kh, Vh = (t[0, h].float().cpu().numpy() for t in (q, k, v))
+        qc, qs = O.quantize_int8_blocks(Qh, L)
+        assert np.array_equal(views["q8"][0, h].cpu().numpy(), qc)
+        assert np.array_equal(views["q_scale"][0, h].cpu().numpy(), qs)
+        counts = masks[0, h].sum(1)
+        blocks = sorted({0, L.n - 1, int(np.argmax(counts)), int(rng.integers(0, L.n))})
+        outs, lses = O.quantized_attention_rows(Qh, Kh, Vh, masks[0, h], L, blocks)
+        og, lg = o[0, h].float().cpu().numpy(), lse[0, h].cpu().numpy()
+        for i, orf, lrf in zip(blocks, outs, lses):
+            lo, hi = L.block_range(i)
+            errs.append(np.abs(og[lo:hi] - orf).ravel())
+            assert np.max(np.abs(lg[lo:hi] - lrf)) <= LSE_ABS
+    d = np.concatenate(errs)
+    assert d.max() <= MAX_ABS and d.mean() <= MEAN_ABS, (d.max(), d.mean())
