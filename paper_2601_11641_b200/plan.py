@@ -76,6 +76,8 @@ class Plan:
         self.min_pivot, self.null_dim = mp.value, nd.value
         self.ws_bytes = lib.mod_plan_workspace_bytes(h)
         self._ws = None
+        # softmax scale s: 1/sqrt(head_dim) unless given
+        self.scale = softmax_scale if softmax_scale > 0 else 1.0 / float(self.spec.head_dim) ** 0.5
 
     # ------------------------------------------------------------------ plumbing
     def __del__(self):

@@ -86,3 +86,28 @@ def test_schedule_q8_same_masks_as_bf16():
             assert d.max().item() <= 0.1 and d.mean().item() <= 6e-3
     with pytest.raises(ValueError, match="stat='pooled'"):
         Schedule(P, precision="q8", stat="exact")
+
+
+def test_schedule_sdpa_warmup_same_masks():
+    """warmup_attention='sdpa' (library dense kernel for the full-attention warm-up, as the paper's FA2)
+    leaves the pooled statistics -- hence every mask -- unchanged, and its warm-up output matches K4's."""
+    import paper_2601_11641_b200 as M
+    from paper_2601_11641_b200.schedule import Schedule
+    w = syn.Workload("small-prefix", 1, 3, 128, 40, 3, 20, 19, 128)
+    P = M.Plan(w, top_k=6)
+    a = Schedule(P, T=20, m=12, dt=10)
+    b = Schedule(P, T=20, m=12, dt=10, warmup_attention="sdpa")
+    for t in range(1, 21):
+        q, k, v = syn.family_s(w, step=t, device="cuda")
+        oa, _ = a.step(t, q, k, v)
+        oa = oa.clone()
+        ob, _ = b.step(t, q, k, v)
+        (ra, ca), (rb, cb) = a.last_mask, b.last_mask
+        assert torch.equal(ra, rb)
+        for h in range(w.heads):
+            nnz = int(ra[0, h, -1])
+            assert torch.equal(ca[0, h, :nnz], cb[0, h, :nnz])
+        d = (oa.float() - ob.float()).abs()
+        assert d.max().item() <= 2e-2
+    with pytest.raises(ValueError, match="stat='pooled'"):
+        Schedule(P, warmup_attention="sdpa", stat="exact")
