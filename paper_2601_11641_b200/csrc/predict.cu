@@ -10,8 +10,8 @@
 //  3. block mask = selected diagonals (j - i = delta_k) | selected columns | kept frame squares
 //     [a_r,b_r]^2 | diagonal guard | prefix rows/columns (Alg. 1; Z15, Z17),
 //     emitted as a CSR index list.  Steps 1 (one CTA per head), 2 (row counts) and 3 (row
-//     pointers + column lists) are separate launches so that the O(n^2) mask work spreads over
-//     (row chunk, head) CTAs: a warp per row, ballot + popc for counts and write positions.
+//     pointers + column lists) are separate launches so that the mask work spreads over
+//     (row chunk, head) CTAs: a warp per row, 32 columns per lane-word built from bit strings.
 #include "common.cuh"
 
 namespace {
@@ -119,57 +119,86 @@ __global__ void __launch_bounds__(1024) select_kernel(PredictArgs a) {
 
 constexpr int kRowsPerCta = 32;   // 8 warps x 4 rows
 
-struct RowCtx {
-  const uint8_t* selC;   // smem [2n-1], index j - i + n - 1
-  const uint8_t* selD;   // smem [n]
-  const uint8_t* keep;   // global [F] or null
+// The passing set of row i is a union of shifted / fixed bit strings: the selected
+// diagonals are the C selection bits read through a window that slides with i, the selected columns
+// the D selection bits, kept frame squares and the prefix contiguous ranges, the guard one bit.
+// Rows are therefore built 32 columns per lane-word (funnel shift + range masks) instead of testing
+// the n columns one by one.
+struct RowBits {
+  const uint32_t* cbits;   // smem: bit k = C_k selected (k in [0, 2n-1)), zero padded
+  const uint32_t* dbits;   // smem: bit j = D_j selected
+  const uint8_t* keep;     // global [F] or null
   const int* frame_ab;
   const int* row_frames;
   int n, prefix_last, diag_guard;
-  __device__ __forceinline__ bool pass(int i, int j) const {
-    if (selC[j - i + n - 1] || selD[j]) return true;
-    if (diag_guard && i == j) return true;
-    if (i <= prefix_last || j <= prefix_last) return true;
-    if (keep) {
-      const int rlo = row_frames[2 * i], rhi = row_frames[2 * i + 1];
-      for (int r = rlo; r <= rhi; ++r)
-        if (keep[r] && frame_ab[2 * r] <= j && j <= frame_ab[2 * r + 1]) return true;
-    }
-    return false;
-  }
 };
 
-__device__ __forceinline__ RowCtx load_row_ctx(const PredictArgs& a, uint8_t* s_sel, size_t bh) {
-  const int P = 3 * a.n - 1;
+__device__ __forceinline__ uint32_t range_bits(int a, int b, int j0) {   // bits of [a, b] in word [j0, j0+32)
+  const int lo = max(a, j0), hi = min(b, j0 + 31);
+  if (lo > hi) return 0u;
+  return (0xffffffffu >> (31 - (hi - lo))) << (lo - j0);
+}
+
+__device__ __forceinline__ uint32_t row_word(const RowBits& c, int i, int w) {
+  const int n = c.n, j0 = 32 * w;
+  if (j0 >= n) return 0u;
+  uint32_t m = c.dbits[w];
+  const int o = n - 1 - i + j0;                 // C bit of column j0: delta = j0 - i
+  m |= __funnelshift_r(c.cbits[o >> 5], c.cbits[(o >> 5) + 1], o & 31);
+  if (c.diag_guard && (i >> 5) == w) m |= 1u << (i & 31);
+  if (c.prefix_last >= 0) m |= (i <= c.prefix_last) ? 0xffffffffu : range_bits(0, c.prefix_last, j0);
+  if (c.keep) {
+    const int rlo = c.row_frames[2 * i], rhi = c.row_frames[2 * i + 1];
+    for (int r = rlo; r <= rhi; ++r)
+      if (c.keep[r]) m |= range_bits(c.frame_ab[2 * r], c.frame_ab[2 * r + 1], j0);
+  }
+  if (j0 + 32 > n) m &= (1u << (n - j0)) - 1u;
+  return m;
+}
+
+// selection bytes of head bh -> bit strings in shared memory (warp per word, ballot)
+__device__ __forceinline__ RowBits load_row_bits(const PredictArgs& a, uint32_t* s_bits, size_t bh) {
+  const int n = a.n, P = 3 * n - 1;
+  const int wc = (2 * n + 63) / 32 + 1, wd = (n + 31) / 32;
   const uint8_t* g = a.sel + bh * P;
-  for (int e = threadIdx.x; e < P; e += blockDim.x) s_sel[e] = g[e];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  for (int w = warp; w < wc + wd; w += nw) {
+    bool bit;
+    if (w < wc) {
+      const int k = 32 * w + lane;
+      bit = k < 2 * n - 1 && g[k];
+    } else {
+      const int j = 32 * (w - wc) + lane;
+      bit = j < n && g[2 * n - 1 + j];
+    }
+    const uint32_t m = __ballot_sync(0xffffffffu, bit);
+    if (lane == 0) s_bits[w] = m;
+  }
   __syncthreads();
-  RowCtx c;
-  c.selC = s_sel;
-  c.selD = s_sel + 2 * a.n - 1;
+  RowBits c;
+  c.cbits = s_bits;
+  c.dbits = s_bits + wc;
   c.keep = a.keep ? a.keep + bh * a.F : nullptr;
   c.frame_ab = a.frame_ab;
   c.row_frames = a.row_frames;
-  c.n = a.n;
+  c.n = n;
   c.prefix_last = a.prefix_last;
   c.diag_guard = a.diag_guard;
   return c;
 }
 
-// 2. passing blocks per row (warp per row, ballot + popc)
+// 2. passing blocks per row: warp per row, lane-words of 32 columns (n <= 2048: <= 2 words per lane)
 __global__ void __launch_bounds__(256) count_kernel(PredictArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const size_t bh = blockIdx.y;
-  const RowCtx c = load_row_ctx(a, smem, bh);
+  const RowBits c = load_row_bits(a, reinterpret_cast<uint32_t*>(smem), bh);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, n = a.n;
   for (int r = 0; r < kRowsPerCta / 8; ++r) {
     const int i = blockIdx.x * kRowsPerCta + warp * (kRowsPerCta / 8) + r;
     if (i >= n) break;
-    int cnt = 0;
-    for (int j0 = 0; j0 < n; j0 += 32) {
-      const int j = j0 + lane;
-      cnt += __popc(__ballot_sync(0xffffffffu, j < n && c.pass(i, j)));
-    }
+    int cnt = __popc(row_word(c, i, lane)) + __popc(row_word(c, i, lane + 32));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
     if (lane == 0) a.cnt[bh * n + i] = cnt;
   }
 }
@@ -180,7 +209,7 @@ __global__ void __launch_bounds__(256) write_kernel(PredictArgs a) {
   __shared__ int red[8];
   __shared__ int rowoff[kRowsPerCta + 1];
   const size_t bh = blockIdx.y;
-  const RowCtx c = load_row_ctx(a, smem, bh);
+  const RowBits c = load_row_bits(a, reinterpret_cast<uint32_t*>(smem), bh);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, n = a.n;
   const int i0 = blockIdx.x * kRowsPerCta;
   const int* cnt = a.cnt + bh * n;
@@ -208,12 +237,24 @@ __global__ void __launch_bounds__(256) write_kernel(PredictArgs a) {
     const int i = i0 + rr;
     if (i >= n) break;
     int pos = rowoff[rr];
-    for (int j0 = 0; j0 < n; j0 += 32) {
-      const int j = j0 + lane;
-      const bool ps = j < n && c.pass(i, j);
-      const unsigned m = __ballot_sync(0xffffffffu, ps);
-      if (ps) ci[pos + __popc(m & ((1u << lane) - 1u))] = j;
-      pos += __popc(m);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {   // words 0..31, then 32..63: ascending columns
+      uint32_t m = row_word(c, i, lane + 32 * h);
+      const int pc = __popc(m);
+      int incl = pc;                 // inclusive warp scan of the lane counts
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int q = pos + incl - pc;
+      const int j0 = 32 * (lane + 32 * h);
+      while (m) {
+        const int b = __ffs(m) - 1;
+        ci[q++] = j0 + b;
+        m &= m - 1u;
+      }
+      pos += __shfl_sync(0xffffffffu, incl, 31);
     }
   }
 }
@@ -271,7 +312,7 @@ extern "C" mod_status mod_predict_block_mask(mod_plan P, const double* x_prev, c
   select_kernel<<<BH, 1024, smem, s>>>(a);
   MOD_LAUNCH_CHECK();
   const dim3 rg((P->n + kRowsPerCta - 1) / kRowsPerCta, BH);
-  const size_t rsm = (size_t)(3 * P->n + 16);
+  const size_t rsm = (size_t)((2 * P->n + 63) / 32 + 1 + (P->n + 31) / 32) * sizeof(uint32_t);
   count_kernel<<<rg, 256, rsm, s>>>(a);
   MOD_LAUNCH_CHECK();
   write_kernel<<<rg, 256, rsm, s>>>(a);
