@@ -35,6 +35,22 @@ __global__ void __launch_bounds__(128, 1) k(long long* cyc, int niter) {
       }
     }
   }
+  if ((MODE == 10 || MODE == 11) && threadIdx.x >= 32) {
+    // warps 1-3: back-to-back 4 x LDTM.x32 bursts (a softmax warp reading its 128-column S row)
+    const int w = threadIdx.x / 32;
+    const uint32_t base = tmem + ((uint32_t)(w * 32) << 16) + 256;
+    uint32_t r[4][32];
+    uint32_t acc = 0;
+    while (!stop_flag) {
+      tmem_ld32(base, r[0]);
+      tmem_ld32(base + 32, r[1]);
+      tmem_ld32(base + 64, r[2]);
+      tmem_ld32(base + 96, r[3]);
+      tmem_ld_wait();
+      acc += r[0][0] + r[1][5] + r[2][9] + r[3][31];
+    }
+    if (acc == 0x12345678u) cyc[0] = acc;
+  }
   if ((MODE == 6 || MODE == 7) && threadIdx.x >= 32) {
     // warps 1-3: lane quarters 1-3, columns [256, 384): ld 32 columns, st them back, repeat
     const int w = threadIdx.x / 32;
@@ -74,7 +90,7 @@ __global__ void __launch_bounds__(128, 1) k(long long* cyc, int niter) {
       for (int kk = 0; kk < 8; ++kk) {
         const uint64_t bd = MODE == 1 ? smem_desc_sw128(sb + kk * 2048, 128 * 128, 1024)
                                       : smem_desc_sw128(sb + (kk / 4) * (N * 128) + (kk % 4) * 32, 16, 1024);
-        if (TS || MODE == 7 || MODE == 9) mma_ts(tmem, tmem + 384 + kk * 8, bd, idesc, 1u);
+        if (TS || MODE == 7 || MODE == 9 || MODE == 11) mma_ts(tmem, tmem + 384 + kk * 8, bd, idesc, 1u);
         else if (MODE >= 3) {
           const uint64_t ad = smem_desc_sw128(sa + (kk / 4) * 16384 + (kk % 4) * 32, 16, 1024);
           mma_ss(tmem, ad, bd, idesc, 1u);
@@ -132,5 +148,7 @@ int main() {
   run<128, false, 7>("TS + TMEM ld/st");
   run<128, false, 8>("SS + smem stores");
   run<128, false, 9>("TS + smem stores");
+  run<128, false, 10>("SS + LDTM bursts");
+  run<128, false, 11>("TS + LDTM bursts");
   return 0;
 }
