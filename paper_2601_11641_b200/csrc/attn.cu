@@ -26,6 +26,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -348,6 +349,334 @@ __global__ void __launch_bounds__(320, 1)
   }
 }
 
+// ================================================================================================
+// Paired query blocks: one CTA per (b, h, pair of query blocks 2p, 2p+1).
+// Adjacent rows of the MOD-DiT mask share most of their index lists (vertical columns, frame
+// squares, diagonals whose neighbour offset is also selected: 79 % at Hunyuan 720p, Family S), so the
+// two query tiles A = block 2p and B = block 2p+1 walk the MERGED list ("stream") of their columns:
+// each stream entry's K/V tile is fetched ONCE and feeds S and PV of every tile whose list holds it.
+// FLOPs are exactly those of the selected blocks (a column in one list only is computed for that
+// tile only), while L2->SMEM K/V traffic and TMA/barrier work per block drop by the shared fraction.
+//   warp 0      producer: Q_A, Q_B once; then K(u), V(u) for stream entries u (K one entry ahead).
+//   warp 1      single-thread tcgen05 issuer.  Per stream entry u, for each tile X holding u:
+//                  [wait P_X(prev)] PV_X(prev) -> O_X ;  S_X(u) = Q_X K(u)^T -> S_X
+//               (the FA4-style interleave when both tiles hold u; the single kernel's split-KV order
+//               when the lists alternate).  A PV still pending two entries back is issued first, so
+//               its V slot can be refilled (no deadlock however the lists interleave).
+//   warps 2..5  softmax of tile A, warps 6..9 softmax of tile B (thread = query row), as in the
+//               single kernel; P overwrites S_X in TMEM; each tile owns O_X, so no split-KV merge.
+// TMEM: S_A [0,BN), S_B [BN,2BN), O_A [2BN,2BN+D), O_B [2BN+D,2BN+2D).
+template <int D, int BN>
+struct PairCfg {
+  static constexpr int BM = 128;
+  static constexpr int Q_BOX = BM * 128, KV_BOX = BN * 128, NATOM = D / 64;
+  static constexpr int Q_BYTES = Q_BOX * NATOM, KV_BYTES = KV_BOX * NATOM;
+  static constexpr int OFF_Q = 0;                          // Q_A, Q_B
+  static constexpr int OFF_K = OFF_Q + 2 * Q_BYTES;       // 2 slots, slot = u & 1
+  static constexpr int OFF_V = OFF_K + 2 * KV_BYTES;      // 2 slots, slot = u & 1
+  static constexpr int OFF_BAR = OFF_V + 2 * KV_BYTES;
+  // q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], p_full[2], o_done[2], tmem slot
+  static constexpr int NUM_BARS = 1 + 2 * 7;
+  static constexpr int OFF_LIST = OFF_BAR + NUM_BARS * 8 + 16;   // uint16 columns of A then B
+  static constexpr int MAX_LIST = (232448 - OFF_LIST) / 4;       // per tile
+  static constexpr int SMEM_BASE = OFF_LIST;
+  static constexpr int TMEM_S = 0, TMEM_O = 2 * BN;
+  static constexpr uint32_t TMEM_COLS = (2 * BN + 2 * D) <= 256 ? 256 : 512;
+  static constexpr uint32_t IDESC_S = idesc_bf16_f32(BM, BN, false, false);
+  static constexpr uint32_t IDESC_O = idesc_bf16_f32(BM, D, false, true);
+  static constexpr int THREADS = 320;
+};
+
+template <int D, int BN>
+__global__ void __launch_bounds__(320, 1)
+    attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                     const __grid_constant__ CUtensorMap tm_v, const int* __restrict__ row_ptr,
+                     const int* __restrict__ col_idx, __nv_bfloat16* __restrict__ out, float* __restrict__ lse,
+                     int N, int n, float scale_log2, int dbg) {
+  using C = PairCfg<D, BN>;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = bars + 1;
+  uint64_t* k_empty = k_full + 2;
+  uint64_t* v_full = k_empty + 2;
+  uint64_t* v_empty = v_full + 2;
+  uint64_t* s_full = v_empty + 2;   // [tile]
+  uint64_t* p_full = s_full + 2;    // [tile]
+  uint64_t* o_done = p_full + 2;    // [tile]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+  uint16_t* lists = reinterpret_cast<uint16_t*>(smem + C::OFF_LIST);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int npair = (n + 1) >> 1;
+  const int bh = blockIdx.x / npair, qa = 2 * (blockIdx.x % npair), qb = qa + 1;
+  const int* rp = row_ptr + (size_t)bh * (n + 1);
+  const int begA = rp[qa], LA = rp[qa + 1] - begA;
+  const int begB = qb < n ? rp[qb] : 0, LB = qb < n ? rp[qb + 1] - begB : 0;
+  const int* colsA = col_idx + (size_t)bh * n * n + begA;
+  const int* colsB = col_idx + (size_t)bh * n * n + begB;
+  uint16_t* la = lists;
+  uint16_t* lb = lists + LA;
+  for (int t = threadIdx.x; t < LA + LB; t += blockDim.x) lists[t] = (uint16_t)(t < LA ? colsA[t] : colsB[t - LA]);
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+      mbar_init(&s_full[s], 1);
+      mbar_init(&p_full[s], 128);
+      mbar_init(&o_done[s], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const bool any = LA + LB > 0;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (stream order)
+    if (lane == 0 && any) {
+      tma_prefetch_desc(&tm_q);
+      tma_prefetch_desc(&tm_k);
+      tma_prefetch_desc(&tm_v);
+      const uint64_t pol_q = policy_evict_first(), pol_kv = policy_evict_last();
+      mbar_arrive_expect_tx(q_full, (LB > 0 ? 2 : 1) * C::Q_BYTES);
+#pragma unroll
+      for (int a = 0; a < C::NATOM; ++a)
+        tma_load_3d(smem + C::OFF_Q + a * C::Q_BOX, &tm_q, q_full, a * 64, qa * BN, bh, pol_q);
+      if (LB > 0) {
+#pragma unroll
+        for (int a = 0; a < C::NATOM; ++a)
+          tma_load_3d(smem + C::OFF_Q + C::Q_BYTES + a * C::Q_BOX, &tm_q, q_full, a * 64, qb * BN, bh, pol_q);
+      }
+      auto load = [&](uint64_t* full, uint64_t* empty, int off, const CUtensorMap* tm, int u, int col) {
+        const int s = u & 1;
+        if (u >= 2) mbar_wait(&empty[s], ((u >> 1) - 1) & 1);   // entry u-2 released the slot
+        unsigned char* dst = smem + off + s * C::KV_BYTES;
+        mbar_arrive_expect_tx(&full[s], C::KV_BYTES);
+#pragma unroll
+        for (int a = 0; a < C::NATOM; ++a) tma_load_3d(dst + a * C::KV_BOX, tm, &full[s], a * 64, col * BN, bh, pol_kv);
+      };
+      // walk the merged stream; K runs one entry ahead of V (the issuer's demand order)
+      int ia = 0, ib = 0, u = 0, vcol_prev = -1;
+      while (ia < LA || ib < LB) {
+        const int ca = ia < LA ? la[ia] : 0x7fffffff, cb = ib < LB ? lb[ib] : 0x7fffffff;
+        const int c = min(ca, cb);
+        ia += ca == c;
+        ib += cb == c;
+        load(k_full, k_empty, C::OFF_K, &tm_k, u, c);
+        if (u >= 1) load(v_full, v_empty, C::OFF_V, &tm_v, u - 1, vcol_prev);
+        vcol_prev = c;
+        ++u;
+      }
+      load(v_full, v_empty, C::OFF_V, &tm_v, u - 1, vcol_prev);
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0 && any) {
+      const uint32_t sq = smem_u32(smem + C::OFF_Q);
+      mbar_wait(q_full, 0);
+      // scalar state (no dynamically indexed arrays: they would live in local memory)
+      int tc_ = 0;
+      int pend0 = -1, pend1 = -1;      // stream entry of tile X's issued S whose PV is still due
+      int npv0 = 0, npv1 = 0;          // PVs issued per tile (phase of p_full[X])
+      int vrem0 = 0, vrem1 = 0;        // PVs still to read V slot 0 / 1
+      auto emit_pv = [&](int X) {
+        const int e = X ? pend1 : pend0, s = e & 1;
+        const int np = X ? npv1 : npv0;
+        mbar_wait(&v_full[s], (e >> 1) & 1);
+        mbar_wait(&p_full[X], np & 1);
+        trace(dbg, 1, tc_, 12 + 2 * X, e);
+        tc_fence_after();
+        const uint32_t sv = smem_u32(smem + C::OFF_V + s * C::KV_BYTES);
+        const uint32_t p_t = tmem + C::TMEM_S + X * BN;
+#pragma unroll
+        for (int kk = 0; kk < BN / 16; ++kk) {
+          const uint64_t bd = smem_desc_sw128(sv + kk * 2048, C::KV_BOX, 1024);
+          mma_ts(tmem + C::TMEM_O + X * D, p_t + kk * 8, bd, C::IDESC_O, (np > 0 || kk > 0) ? 1u : 0u);
+        }
+        mma_commit(&o_done[X]);
+        const int left = s ? --vrem1 : --vrem0;
+        if (left == 0) mma_commit(&v_empty[s]);
+        if (X) { pend1 = -1; ++npv1; } else { pend0 = -1; ++npv0; }
+      };
+      bool kwait = false;              // K(u) already waited for by this entry's first S
+      auto emit_s = [&](int X, int u) {
+        if (!kwait) {
+          mbar_wait(&k_full[u & 1], (u >> 1) & 1);
+          kwait = true;
+        }
+        const uint32_t sk = smem_u32(smem + C::OFF_K + (u & 1) * C::KV_BYTES);
+        const uint32_t qx = sq + X * C::Q_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint64_t ad = smem_desc_sw128(qx + (kk / 4) * C::Q_BOX + (kk % 4) * 32, 16, 1024);
+          const uint64_t bd = smem_desc_sw128(sk + (kk / 4) * C::KV_BOX + (kk % 4) * 32, 16, 1024);
+          mma_ss(tmem + C::TMEM_S + X * BN, ad, bd, C::IDESC_S, kk > 0 ? 1u : 0u);
+        }
+        mma_commit(&s_full[X]);
+        if (X) pend1 = u; else pend0 = u;
+      };
+      // the older pending PV first (V slots drain in stream order); only those at or before `lim`
+      auto drain = [&](int lim) {
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const bool x0 = pend0 >= 0 && (pend1 < 0 || pend0 <= pend1);
+          const int e = x0 ? pend0 : pend1;
+          if (e >= 0 && e <= lim) emit_pv(x0 ? 0 : 1);
+        }
+      };
+      int ia = 0, ib = 0, u = 0;
+      while (ia < LA || ib < LB) {
+        const int ca = ia < LA ? la[ia] : 0x7fffffff, cb = ib < LB ? lb[ib] : 0x7fffffff;
+        const int c = min(ca, cb);
+        const bool fa = ca == c, fb = cb == c;
+        ia += fa;
+        ib += fb;
+        // V slot (u & 1) is refilled with V(u) once entry u-2's PVs are done: issue any still pending
+        drain(u - 2);
+        if (u & 1) vrem1 = (int)fa + (int)fb; else vrem0 = (int)fa + (int)fb;
+        kwait = false;
+        // FA4-style interleave when both lists hold u: PV_A, S_A(u), PV_B, S_B(u)
+        trace(dbg, 1, tc_, 10, u);
+        if (fa) {
+          if (pend0 >= 0) emit_pv(0);
+          emit_s(0, u);
+        }
+        if (fb) {
+          if (pend1 >= 0) emit_pv(1);
+          emit_s(1, u);
+        }
+        trace(dbg, 1, tc_, 13, u);
+        mma_commit(&k_empty[u & 1]);   // both S of entry u issued: K slot free once they complete
+        ++u;
+      }
+      drain(0x7fffffff);
+    }
+  } else {
+    // ------------------------------------------------------------ softmax / epilogue, tile X = (warp-2)/4
+    const int X = (warp - 2) >> 2;
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const uint32_t t_s = tmem + lane_off + C::TMEM_S + X * BN;
+    const uint32_t t_o = tmem + lane_off + C::TMEM_O + X * D;
+    const int qx = X ? qb : qa;
+    const int LX = X ? LB : LA;
+    const uint16_t* lx = X ? lb : la;
+    float m_run = -INFINITY, l_run = 0.f;
+    int tc_ = 0;
+    for (int j = 0; j < LX; ++j) {
+      mbar_wait(&s_full[X], j & 1);
+      if (lane == 0 && quarter == 2) trace(dbg, 2 + X, tc_, 20 + X, j);
+      tc_fence_after();
+      uint32_t sr[BN];
+#pragma unroll
+      for (int c = 0; c < BN / 32; ++c) tmem_ld32(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
+      tmem_ld_wait();
+      float* s = reinterpret_cast<float*>(sr);
+      const int kv_valid = N - (int)lx[j] * BN;
+      if (kv_valid < BN) {
+#pragma unroll
+        for (int c = 0; c < BN; ++c)
+          if (c >= kv_valid) s[c] = -INFINITY;
+      }
+      float mxv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) mxv[u] = s[u];
+#pragma unroll
+      for (int c = 8; c < BN; c += 8)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) mxv[u] = fmaxf(mxv[u], s[c + u]);
+      const float mx = fmaxf(fmaxf(fmaxf(mxv[0], mxv[1]), fmaxf(mxv[2], mxv[3])),
+                             fmaxf(fmaxf(mxv[4], mxv[5]), fmaxf(mxv[6], mxv[7])));
+      const float m_new = fmaxf(m_run, mx * scale_log2);
+      const bool rescale = (m_new - m_run) > 8.0f;
+      const float m_use = rescale ? m_new : m_run;
+      const float alpha = rescale ? ex2(m_run - m_new) : 1.0f;
+      const float2 sc2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-m_use, -m_use);
+      float2 acc2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      uint32_t pk[BN / 2];
+#pragma unroll
+      for (int c = 0; c < BN; c += 2) {
+        const float2 x = ffma2(make_float2(s[c], s[c + 1]), sc2, nm2);
+        float2 p;
+        if (((c / 2) & 7) < kEmuPairsPer8) {
+          p = ex2_poly2(x);
+        } else {
+          p.x = ex2(x.x);
+          p.y = ex2(x.y);
+        }
+        acc2[(c / 2) & 1] = fadd2(acc2[(c / 2) & 1], p);
+        pk[c / 2] = pack_bf16(p.x, p.y);
+      }
+      l_run = fmaf(l_run, alpha, (acc2[0].x + acc2[0].y) + (acc2[1].x + acc2[1].y));
+      m_run = m_use;
+#pragma unroll
+      for (int c = 0; c < BN / 64; ++c) tmem_st32(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[c * 32]));
+      // S_X(j) was issued after PV_X(j-1), so s_full above already implies O_X holds PV_X(j-1)
+      if (j >= 1 && __any_sync(0xffffffffu, rescale)) {
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t o[32];
+          tmem_ld32(t_o + c * 32, o);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+          tmem_st32(t_o + c * 32, o);
+        }
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&p_full[X]);
+      if (lane == 0 && quarter == 2) trace(dbg, 2 + X, tc_, 40 + X, j);
+    }
+    // epilogue: O_X / l -> bf16, lse (no merge: each tile owns its accumulator)
+    if (qx < n) {
+      const int q_row0 = qx * BN;
+      const bool valid = row < min(BN, N - q_row0);
+      const size_t grow = (size_t)bh * N + q_row0 + row;
+      if (LX > 0) {
+        mbar_wait(&o_done[X], (LX - 1) & 1);
+        tc_fence_after();
+        const float inv = 1.0f / l_run;
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t o[32];
+          tmem_ld32(t_o + c * 32, o);
+          tmem_ld_wait();
+          uint32_t pkd[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            pkd[e] = pack_bf16(__uint_as_float(o[2 * e]) * inv, __uint_as_float(o[2 * e + 1]) * inv);
+          if (valid) {
+            int4* dst = reinterpret_cast<int4*>(out + grow * D + c * 32);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) dst[e] = make_int4(pkd[4 * e], pkd[4 * e + 1], pkd[4 * e + 2], pkd[4 * e + 3]);
+          }
+        }
+        if (valid && lse) lse[grow] = (m_run + __log2f(l_run)) * 0.69314718055994531f;
+      } else if (valid) {
+        int4* dst = reinterpret_cast<int4*>(out + grow * D);
+#pragma unroll
+        for (int e = 0; e < D / 8; ++e) dst[e] = make_int4(0, 0, 0, 0);
+        if (lse) lse[grow] = -INFINITY;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<C::TMEM_COLS>(tmem);
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -396,6 +725,38 @@ mod_status launch(mod_plan P, const void* q, const void* k, const void* v, const
   return MOD_OK;
 }
 
+template <int D>
+mod_status launch_pair(mod_plan P, const void* q, const void* k, const void* v, const int* row_ptr, const int* col_idx,
+                       void* o, float* lse, cudaStream_t s) {
+  using C = PairCfg<D, 128>;
+  const int BH = P->L.batch * P->L.heads;
+  CUtensorMap tq, tk, tv;
+  mod_status st;
+  if ((st = make_map(&tq, q, BH, P->N, D, C::BM)) != MOD_OK) return st;
+  if ((st = make_map(&tk, k, BH, P->N, D, 128)) != MOD_OK) return st;
+  if ((st = make_map(&tv, v, BH, P->N, D, 128)) != MOD_OK) return st;
+  // two index lists of at most n uint16 columns each follow the barriers
+  const int smem = C::SMEM_BASE + 4 * P->n;
+  auto kern = attn_pair_kernel<D, 128>;
+  MOD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const float scale_log2 = P->scale * 1.4426950408889634f;
+  const int npair = (P->n + 1) / 2;
+  static const int dbg = getenv("MOD_ATTN_DEBUG") ? atoi(getenv("MOD_ATTN_DEBUG")) : 0;   // bring-up only
+  kern<<<BH * npair, C::THREADS, smem, s>>>(tq, tk, tv, row_ptr, col_idx, (__nv_bfloat16*)o, lse, P->N, P->n,
+                                            scale_log2, dbg);
+  MOD_LAUNCH_CHECK();
+  return MOD_OK;
+}
+
+// K4 variant: one query block per CTA (default) or paired query blocks (MOD_ATTN_KERNEL=pair; only
+// for 128-token blocks and n within the pair kernel's shared-memory list capacity).  Measured at
+// Hunyuan 720p the two run at the same speed (profiles/r1/README.md, "Paired query blocks").
+bool use_pair_kernel(mod_plan P) {
+  const char* e = getenv("MOD_ATTN_KERNEL");   // read per call: tests switch kernels in-process
+  if (!(e && strcmp(e, "pair") == 0) || P->L.block != 128) return false;
+  const int cap = P->L.head_dim == 128 ? PairCfg<128, 128>::MAX_LIST : PairCfg<64, 128>::MAX_LIST;
+  return P->n <= cap && P->n <= 65535;
+}
 }  // namespace
 
 // bring-up only (not in moddit.h): copies the trace of the last MOD_ATTN_DEBUG&16 launch
@@ -420,7 +781,9 @@ extern "C" mod_status mod_block_sparse_attn_fwd(mod_plan P, const void* q, const
   MOD_REQUIRE(((uintptr_t)o & 15) == 0, MOD_ERR_INPUT, "o must be 16-byte aligned");
   cudaStream_t s = as_stream(stream);
   const int D = P->L.head_dim, BN = P->L.block;
-  if (D == 128 && BN == 128) st = launch<128, 128>(P, q, k, v, row_ptr, col_idx, o, lse, s);
+  if (use_pair_kernel(P)) st = D == 128 ? launch_pair<128>(P, q, k, v, row_ptr, col_idx, o, lse, s)
+                                        : launch_pair<64>(P, q, k, v, row_ptr, col_idx, o, lse, s);
+  else if (D == 128 && BN == 128) st = launch<128, 128>(P, q, k, v, row_ptr, col_idx, o, lse, s);
   else if (D == 64 && BN == 128) st = launch<64, 128>(P, q, k, v, row_ptr, col_idx, o, lse, s);
   else if (D == 128 && BN == 64) st = launch<128, 64>(P, q, k, v, row_ptr, col_idx, o, lse, s);
   else st = launch<64, 64>(P, q, k, v, row_ptr, col_idx, o, lse, s);

@@ -72,6 +72,33 @@ __global__ void __launch_bounds__(128, 1) k(long long* cyc, int niter) {
     const uint32_t sa = smem_u32(smem), sb = smem_u32(smem + 32768);  // B: up to 256 rows x 2 atoms = 64KB
     long long t0 = clock64();
     for (int it = 0; it < niter; ++it) {
+      if (MODE >= 12) {
+        // K4's tensor-pipe sequence per block pair (j even / odd share nothing but the pipe):
+        //   PV_j: A = P_j (bf16, TMEM S[b]), D = O_b;  S_{j+2}: D = S[b] (overwrites what PV_j read).
+        // 12: exactly that (WAR on S[b] right after PV_j);  13: S_{j+2} into a disjoint region (no WAR);
+        // 14: 12 + commit/try_wait(completed)/fence::after before each group (K4's sync points);
+        // 15: 12 + commit after each group, no waits
+        for (int b = 0; b < 2; ++b) {
+          const uint32_t s_b = tmem + b * 128, o_b = tmem + 256 + b * 128;
+          if (MODE == 14) { mbar_wait(&bar_b, 0); tc_fence_after(); }
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint64_t bd = smem_desc_sw128(sb + kk * 2048, 128 * 128, 1024);
+            mma_ts(o_b, s_b + kk * 8, bd, idesc_mn, 1u);
+          }
+          if (MODE == 14 || MODE == 15) mma_commit(&bar_a);
+          if (MODE == 14) { mbar_wait(&bar_b, 0); tc_fence_after(); }
+          const uint32_t d_s = MODE == 13 ? tmem + 64 + b * 128 + 32 : s_b;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint64_t ad = smem_desc_sw128(sa + (kk / 4) * 16384 + (kk % 4) * 32, 16, 1024);
+            const uint64_t bd = smem_desc_sw128(sb + (kk / 4) * (128 * 128) + (kk % 4) * 32, 16, 1024);
+            mma_ss(MODE == 13 ? (b ? tmem + 64 : tmem + 192 + 0) : d_s, ad, bd, idesc, kk > 0 ? 1u : 0u);
+          }
+          if (MODE == 14 || MODE == 15) mma_commit(&bar_a);
+        }
+        continue;
+      }
       if (MODE == 2) {
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
@@ -128,8 +155,8 @@ template <int N, bool TS, int MODE = 0> void run(const char* name) {
   float ms; cudaEventElapsedTime(&ms, e0, e1);
   long long h[148]; cudaMemcpy(h, d, 148 * 8, cudaMemcpyDeviceToHost);
   double avg = 0; for (int i = 0; i < 148; ++i) avg += h[i]; avg /= 148;
-  double flops = (MODE == 2 ? 2 : 1) * 148.0 * niter * 8 * 2.0 * 128 * N * 16;
-  printf("%-14s %s cycles/MMA=%.1f  ideal=%d  TFLOPS=%.0f  (%.3f ms) err=%s\n", name, TS ? "TS" : "SS", avg / (niter * 8.0),
+  double flops = (MODE >= 12 ? 4 : MODE == 2 ? 2 : 1) * 148.0 * niter * 8 * 2.0 * 128 * N * 16;
+  printf("%-14s %s cycles/MMA=%.1f  ideal=%d  TFLOPS=%.0f  (%.3f ms) err=%s\n", name, TS ? "TS" : "SS", avg / (niter * (MODE >= 12 ? 32.0 : MODE == 2 ? 16.0 : 8.0)),
          128 * N / 256, flops / ms / 1e9, ms, cudaGetErrorString(cudaGetLastError()));
 }
 int main() {
@@ -150,5 +177,9 @@ int main() {
   run<128, false, 9>("TS + smem stores");
   run<128, false, 10>("SS + LDTM bursts");
   run<128, false, 11>("TS + LDTM bursts");
+  run<128, false, 12>("K4seq WAR");
+  run<128, false, 13>("K4seq noWAR");
+  run<128, false, 14>("K4seq+sync");
+  run<128, false, 15>("K4seq+commit");
   return 0;
 }

@@ -69,6 +69,8 @@ int main() {
     k<0><<<148, warps * 32>>>(d, 200, 0.127f); cudaDeviceSynchronize();
     k<0><<<148, warps * 32>>>(d, 1000, 0.127f); cudaMemcpy(h, d, 148 * 4, cudaMemcpyDeviceToHost);
     printf("warps/CTA=%2d EMU=0/8: %.0f cycles per row-block per warp\n", warps, h[0]);
+    k<2><<<148, warps * 32>>>(d, 1000, 0.127f); cudaMemcpy(h, d, 148 * 4, cudaMemcpyDeviceToHost);
+    printf("warps/CTA=%2d EMU=2/8: %.0f cycles per row-block per warp\n", warps, h[0]);
     k<3><<<148, warps * 32>>>(d, 1000, 0.127f); cudaMemcpy(h, d, 148 * 4, cudaMemcpyDeviceToHost);
     printf("warps/CTA=%2d EMU=3/8: %.0f cycles per row-block per warp\n", warps, h[0]);
   }
