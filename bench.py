@@ -332,27 +332,54 @@ def run_ours(args):
     dense_flops = 4.0 * D * N * N * w.batch * w.heads
     fastest = min([x for kk, x in dense.items() if isinstance(x, float)], default=None)
 
-    # ---- e2e through the public API with host buffers (pinned), copies inside the timed region
+    # ---- e2e through the public API with host buffers (pinned), copies inside the timed region.
+    # Default path: HeadChunkPipeline overlaps the upload of head chunk c+1, the hot path on chunk c and
+    # the download of chunk c-1 on three streams (every step is per head); the q8 / exact /
+    # Ulysses variants run serially (upload, step, download on one stream).
     e2e = None
     if not args.no_e2e:
         hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
         ho = torch.empty_like(hq).pin_memory()
+        pipelined = not (q8 or exact or seq is not None) and w.batch == 1
+        if pipelined:
+            from paper_2601_11641_b200.pipeline import HeadChunkPipeline
+            chunks = max(c for c in range(1, min(args.e2e_chunks, Hl) + 1) if Hl % c == 0)
+            pipe = HeadChunkPipeline(w, chunks, top_k=1, tau_e=0.0, masked_renorm=True)
+
+            def chunk_step(plan, c, qc, kc, vc, oc):
+                hs = pipe.heads(c)
+                rpc, cic = rp[:, hs], ci[:, hs]
+                plan.predict_block_mask(x_prev0[:, hs], x_curr0[:, hs], M_WARMUP - 1, M_WARMUP, t_step, keep[:, hs],
+                                        top_k=K, out=(rpc, cic))
+                plan.block_sparse_attn_fwd(qc, kc, vc, rpc, cic, out=oc, lse=lse[:, hs])
+                plan.collect_block_stats(qc, kc, out=Wf[:, hs])
+                plan.update_online_mask(Wf[:, hs], rpc, cic, hist[:, hs], xs_prev[:, hs], xs_curr[:, hs])
+
+            pipe.run(hq, hk, hv, ho, chunk_step)        # untimed warm-up of the pipeline
+            torch.cuda.synchronize()
         barrier(ws)
         torch.cuda.synchronize()
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s0.record(stream)
         for _ in range(args.steps):
-            q.copy_(hq, non_blocking=True)
-            k.copy_(hk, non_blocking=True)
-            v.copy_(hv, non_blocking=True)
-            step()
-            ho.copy_(o, non_blocking=True)
+            if pipelined:
+                pipe.run(hq, hk, hv, ho, chunk_step)
+            else:
+                q.copy_(hq, non_blocking=True)
+                k.copy_(hk, non_blocking=True)
+                v.copy_(hv, non_blocking=True)
+                step()
+                ho.copy_(o, non_blocking=True)
         s1.record(stream)
         torch.cuda.synchronize()
         e2e_ms = max_over_ranks(s0.elapsed_time(s1) / args.steps, ws)
         e2e = {"value": round(flops_all / (e2e_ms * 1e-3) / 1e12, 2), "unit": "TFLOPS",
                "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": int(3 * q.numel() * 2 * ws),
-               "d2h_bytes_per_step": int(o.numel() * 2 * ws)}
+               "d2h_bytes_per_step": int(o.numel() * 2 * ws),
+               "pipeline": (f"{chunks} head chunks on 3 streams (upload / hot path / download overlapped)"
+                            if pipelined else "serial (upload, step, download on one stream)")}
+        if pipelined:
+            del pipe
         del hq, hk, hv, ho
 
     # ---- roofline of the dominant kernel (K4): algorithmic FLOPs / event-timed launch duration
@@ -491,6 +518,7 @@ def main():
     ap.add_argument("--sparsity", type=float, default=0.878)
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-chunks", type=int, default=8, help="head chunks of the pipelined e2e leg")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-blocks", type=int, default=4)
