@@ -677,6 +677,224 @@ __global__ void __launch_bounds__(320, 1)
   }
 }
 
+
+// ================================================================================================
+// Two CTAs per SM, one softmax chain each (MOD_ATTN_KERNEL=dual).  The single kernel above holds one
+// query block per SM with two split-KV softmax groups, so each CTA's pipeline fill (Q load, first S,
+// first softmax) and epilogue (last PV, merge, O store) leave the tensor pipe idle; here a CTA owns
+// ONE chain  S_j -> softmax_j -> PV_j -> S_{j+1}  (TMEM: S [0,BN), O [BN,BN+D) = 256 columns; one-slot
+// K and V buffers, refilled while the chain's softmax runs: 96 KB of shared memory), and two CTAs
+// share each SM, so the two chains interleave on the tensor pipe and one CTA's fill / epilogue
+// overlaps the other's steady state.
+template <int D, int BN>
+struct DualCfg {
+  static constexpr int BM = 128;
+  static constexpr int Q_BOX = BM * 128, KV_BOX = BN * 128, NATOM = D / 64;
+  static constexpr int Q_BYTES = Q_BOX * NATOM, KV_BYTES = KV_BOX * NATOM;
+  static constexpr int OFF_Q = 0, OFF_K = Q_BYTES, OFF_V = OFF_K + KV_BYTES, OFF_BAR = OFF_V + KV_BYTES;
+  static constexpr int NUM_BARS = 6;   // q_full, k_full, v_full, s_full, p_full, o_done
+  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;
+  static constexpr int TMEM_S = 0, TMEM_O = BN;
+  static constexpr uint32_t TMEM_COLS = (BN + D) <= 128 ? 128 : 256;
+  static constexpr uint32_t IDESC_S = idesc_bf16_f32(BM, BN, false, false);
+  static constexpr uint32_t IDESC_O = idesc_bf16_f32(BM, D, false, true);
+  static constexpr int THREADS = 192;
+};
+
+template <int D, int BN>
+__global__ void __launch_bounds__(192, 2)
+    attn_dual_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                     const __grid_constant__ CUtensorMap tm_v, const int* __restrict__ row_ptr,
+                     const int* __restrict__ col_idx, __nv_bfloat16* __restrict__ out, float* __restrict__ lse,
+                     int N, int n, int block, float scale_log2) {
+  using C = DualCfg<D, BN>;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = bars + 1;
+  uint64_t* v_full = bars + 2;
+  uint64_t* s_full = bars + 3;
+  uint64_t* p_full = bars + 4;
+  uint64_t* o_done = bars + 5;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int item = blockIdx.x;
+  const int bh = item / n, qi = item % n;
+  const int beg = row_ptr[(size_t)bh * (n + 1) + qi];
+  const int L = row_ptr[(size_t)bh * (n + 1) + qi + 1] - beg;
+  const int* cols = col_idx + (size_t)bh * n * n + beg;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    mbar_init(k_full, 1);
+    mbar_init(v_full, 1);
+    mbar_init(s_full, 1);
+    mbar_init(p_full, 128);
+    mbar_init(o_done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0 && L > 0) {
+      const uint64_t pol_q = policy_evict_first(), pol_kv = policy_evict_last();
+      mbar_arrive_expect_tx(q_full, C::Q_BYTES);
+#pragma unroll
+      for (int a = 0; a < C::NATOM; ++a)
+        tma_load_3d(smem + C::OFF_Q + a * C::Q_BOX, &tm_q, q_full, a * 64, qi * block, bh, pol_q);
+      for (int j = 0; j < L; ++j) {
+        const int row = cols[j] * block;
+        if (j >= 1) mbar_wait(s_full, (j - 1) & 1);   // S_{j-1} has read K_{j-1}
+        mbar_arrive_expect_tx(k_full, C::KV_BYTES);
+#pragma unroll
+        for (int a = 0; a < C::NATOM; ++a) tma_load_3d(smem + C::OFF_K + a * C::KV_BOX, &tm_k, k_full, a * 64, row, bh, pol_kv);
+        if (j >= 1) mbar_wait(o_done, (j - 1) & 1);   // PV_{j-1} has read V_{j-1}
+        mbar_arrive_expect_tx(v_full, C::KV_BYTES);
+#pragma unroll
+        for (int a = 0; a < C::NATOM; ++a) tma_load_3d(smem + C::OFF_V + a * C::KV_BOX, &tm_v, v_full, a * 64, row, bh, pol_kv);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer: S_j, [P_j] PV_j, S_{j+1}, ...
+    if (lane == 0 && L > 0) {
+      const uint32_t sq = smem_u32(smem + C::OFF_Q), sk = smem_u32(smem + C::OFF_K), sv = smem_u32(smem + C::OFF_V);
+      mbar_wait(q_full, 0);
+      for (int j = 0; j < L; ++j) {
+        mbar_wait(k_full, j & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint64_t ad = smem_desc_sw128(sq + (kk / 4) * C::Q_BOX + (kk % 4) * 32, 16, 1024);
+          const uint64_t bd = smem_desc_sw128(sk + (kk / 4) * C::KV_BOX + (kk % 4) * 32, 16, 1024);
+          mma_ss(tmem + C::TMEM_S, ad, bd, C::IDESC_S, kk > 0 ? 1u : 0u);
+        }
+        mma_commit(s_full);
+        mbar_wait(v_full, j & 1);
+        mbar_wait(p_full, j & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < BN / 16; ++kk) {
+          const uint64_t bd = smem_desc_sw128(sv + kk * 2048, C::KV_BOX, 1024);
+          mma_ts(tmem + C::TMEM_O, tmem + C::TMEM_S + kk * 8, bd, C::IDESC_O, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        mma_commit(o_done);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ softmax / epilogue (warps 2..5)
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const uint32_t t_s = tmem + lane_off + C::TMEM_S;
+    const uint32_t t_o = tmem + lane_off + C::TMEM_O;
+    const int q_row0 = qi * block;
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int j = 0; j < L; ++j) {
+      mbar_wait(s_full, j & 1);
+      tc_fence_after();
+      uint32_t sr[BN];
+#pragma unroll
+      for (int c = 0; c < BN / 32; ++c) tmem_ld32(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
+      tmem_ld_wait();
+      float* s = reinterpret_cast<float*>(sr);
+      const int kv_valid = N - cols[j] * block;
+      if (kv_valid < BN) {
+#pragma unroll
+        for (int c = 0; c < BN; ++c)
+          if (c >= kv_valid) s[c] = -INFINITY;
+      }
+      float mxv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) mxv[u] = s[u];
+#pragma unroll
+      for (int c = 8; c < BN; c += 8)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) mxv[u] = fmaxf(mxv[u], s[c + u]);
+      const float mx = fmaxf(fmaxf(fmaxf(mxv[0], mxv[1]), fmaxf(mxv[2], mxv[3])),
+                             fmaxf(fmaxf(mxv[4], mxv[5]), fmaxf(mxv[6], mxv[7])));
+      const float m_new = fmaxf(m_run, mx * scale_log2);
+      const bool rescale = (m_new - m_run) > 8.0f;
+      const float m_use = rescale ? m_new : m_run;
+      const float alpha = rescale ? ex2(m_run - m_new) : 1.0f;
+      const float2 sc2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-m_use, -m_use);
+      float2 acc2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      uint32_t pk[BN / 2];
+#pragma unroll
+      for (int c = 0; c < BN; c += 2) {
+        const float2 x = ffma2(make_float2(s[c], s[c + 1]), sc2, nm2);
+        float2 p;
+        if (((c / 2) & 7) < kEmuPairsPer8) {
+          p = ex2_poly2(x);
+        } else {
+          p.x = ex2(x.x);
+          p.y = ex2(x.y);
+        }
+        acc2[(c / 2) & 1] = fadd2(acc2[(c / 2) & 1], p);
+        pk[c / 2] = pack_bf16(p.x, p.y);
+      }
+      l_run = fmaf(l_run, alpha, (acc2[0].x + acc2[0].y) + (acc2[1].x + acc2[1].y));
+      m_run = m_use;
+#pragma unroll
+      for (int c = 0; c < BN / 64; ++c) tmem_st32(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[c * 32]));
+      // S_j was issued after PV_{j-1}: s_full above already implies O holds PV_{j-1}
+      if (j >= 1 && __any_sync(0xffffffffu, rescale)) {
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t o[32];
+          tmem_ld32(t_o + c * 32, o);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+          tmem_st32(t_o + c * 32, o);
+        }
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(p_full);
+    }
+    const bool valid = row < min(block, N - q_row0);
+    const size_t grow = (size_t)bh * N + q_row0 + row;
+    if (L > 0) {
+      mbar_wait(o_done, (L - 1) & 1);
+      tc_fence_after();
+      const float inv = 1.0f / l_run;
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t o[32];
+        tmem_ld32(t_o + c * 32, o);
+        tmem_ld_wait();
+        uint32_t pkd[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          pkd[e] = pack_bf16(__uint_as_float(o[2 * e]) * inv, __uint_as_float(o[2 * e + 1]) * inv);
+        if (valid) {
+          int4* dst = reinterpret_cast<int4*>(out + grow * D + c * 32);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) dst[e] = make_int4(pkd[4 * e], pkd[4 * e + 1], pkd[4 * e + 2], pkd[4 * e + 3]);
+        }
+      }
+      if (valid && lse) lse[grow] = (m_run + __log2f(l_run)) * 0.69314718055994531f;
+    } else if (valid) {
+      int4* dst = reinterpret_cast<int4*>(out + grow * D);
+#pragma unroll
+      for (int e = 0; e < D / 8; ++e) dst[e] = make_int4(0, 0, 0, 0);
+      if (lse) lse[grow] = -INFINITY;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<C::TMEM_COLS>(tmem);
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -757,6 +975,30 @@ bool use_pair_kernel(mod_plan P) {
   const int cap = P->L.head_dim == 128 ? PairCfg<128, 128>::MAX_LIST : PairCfg<64, 128>::MAX_LIST;
   return P->n <= cap && P->n <= 65535;
 }
+
+template <int D, int BN>
+mod_status launch_dual(mod_plan P, const void* q, const void* k, const void* v, const int* row_ptr, const int* col_idx,
+                       void* o, float* lse, cudaStream_t s) {
+  using C = DualCfg<D, BN>;
+  const int BH = P->L.batch * P->L.heads;
+  CUtensorMap tq, tk, tv;
+  mod_status st;
+  if ((st = make_map(&tq, q, BH, P->N, D, C::BM)) != MOD_OK) return st;
+  if ((st = make_map(&tk, k, BH, P->N, D, BN)) != MOD_OK) return st;
+  if ((st = make_map(&tv, v, BH, P->N, D, BN)) != MOD_OK) return st;
+  auto kern = attn_dual_kernel<D, BN>;
+  MOD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+  const float scale_log2 = P->scale * 1.4426950408889634f;
+  kern<<<BH * P->n, C::THREADS, C::SMEM, s>>>(tq, tk, tv, row_ptr, col_idx, (__nv_bfloat16*)o, lse, P->N, P->n,
+                                              P->L.block, scale_log2);
+  MOD_LAUNCH_CHECK();
+  return MOD_OK;
+}
+
+bool use_dual_kernel() {
+  const char* e = getenv("MOD_ATTN_KERNEL");
+  return e && strcmp(e, "dual") == 0;
+}
 }  // namespace
 
 // bring-up only (not in moddit.h): copies the trace of the last MOD_ATTN_DEBUG&16 launch
@@ -781,7 +1023,12 @@ extern "C" mod_status mod_block_sparse_attn_fwd(mod_plan P, const void* q, const
   MOD_REQUIRE(((uintptr_t)o & 15) == 0, MOD_ERR_INPUT, "o must be 16-byte aligned");
   cudaStream_t s = as_stream(stream);
   const int D = P->L.head_dim, BN = P->L.block;
-  if (use_pair_kernel(P)) st = D == 128 ? launch_pair<128>(P, q, k, v, row_ptr, col_idx, o, lse, s)
+  if (use_dual_kernel()) {
+    if (D == 128 && BN == 128) st = launch_dual<128, 128>(P, q, k, v, row_ptr, col_idx, o, lse, s);
+    else if (D == 64 && BN == 128) st = launch_dual<64, 128>(P, q, k, v, row_ptr, col_idx, o, lse, s);
+    else if (D == 128 && BN == 64) st = launch_dual<128, 64>(P, q, k, v, row_ptr, col_idx, o, lse, s);
+    else st = launch_dual<64, 64>(P, q, k, v, row_ptr, col_idx, o, lse, s);
+  } else if (use_pair_kernel(P)) st = D == 128 ? launch_pair<128>(P, q, k, v, row_ptr, col_idx, o, lse, s)
                                         : launch_pair<64>(P, q, k, v, row_ptr, col_idx, o, lse, s);
   else if (D == 128 && BN == 128) st = launch<128, 128>(P, q, k, v, row_ptr, col_idx, o, lse, s);
   else if (D == 64 && BN == 128) st = launch<64, 128>(P, q, k, v, row_ptr, col_idx, o, lse, s);

@@ -1,5 +1,6 @@
-"""K4 kernel variants against the fp64 oracle: the paired-query-block kernel (default for 128-token
-blocks) and the one-block-per-CTA kernel (MOD_ATTN_KERNEL=single).
+"""K4 kernel variants against the fp64 oracle: the one-block-per-CTA kernel (default), the
+paired-query-block kernel (MOD_ATTN_KERNEL=pair) and the two-CTAs-per-SM
+single-chain kernel (MOD_ATTN_KERNEL=dual).
 
 The pair kernel walks the merged index list of query blocks 2p and 2p+1 and shares each K/V tile
 between them, so its masks are chosen to exercise every shape of that merge: lists that coincide,
@@ -29,7 +30,7 @@ def M():
     return m
 
 
-@pytest.fixture(params=["pair", "single"])
+@pytest.fixture(params=["pair", "single", "dual"])
 def kernel(request, monkeypatch):
     monkeypatch.setenv("MOD_ATTN_KERNEL", request.param)
     return request.param
@@ -128,7 +129,7 @@ def test_pair_and_single_agree_on_structured_masks(M, monkeypatch):
         masks[0, h] = O.block_mask(sel, rng.random(L.frames) < 0.7, L, True)
     rp, ci = masks_to_csr(masks)
     res = {}
-    for kern in ("pair", "single"):
+    for kern in ("pair", "single", "dual"):
         monkeypatch.setenv("MOD_ATTN_KERNEL", kern)
         res[kern] = P.block_sparse_attn_fwd(q, k, v, rp, ci)
     torch.cuda.synchronize()
@@ -136,10 +137,12 @@ def test_pair_and_single_agree_on_structured_masks(M, monkeypatch):
         _check(*res[kern], masks, q, k, v, L)
     # different accumulation orders (split-KV merge vs one accumulator): close, not bitwise
     assert (res["pair"][0].float() - res["single"][0].float()).abs().max().item() <= 2e-2
+    assert (res["dual"][0].float() - res["single"][0].float()).abs().max().item() <= 2e-2
 
 
-def test_pair_deterministic(M, monkeypatch):
-    monkeypatch.setenv("MOD_ATTN_KERNEL", "pair")
+@pytest.mark.parametrize("kern", ["pair", "dual"])
+def test_variant_deterministic(M, monkeypatch, kern):
+    monkeypatch.setenv("MOD_ATTN_KERNEL", kern)
     w = COG_SMALL
     L = olayout(w)
     P = M.Plan(w)
@@ -150,3 +153,19 @@ def test_pair_deterministic(M, monkeypatch):
     o2, l2 = P.block_sparse_attn_fwd(q, k, v, rp, ci)
     torch.cuda.synchronize()
     assert torch.equal(o1, o2) and torch.equal(l1, l2)
+
+
+@pytest.mark.parametrize("w", [syn.TINY], ids=lambda w: w.name)
+def test_dual_block64(M, monkeypatch, w):
+    """The dual kernel also serves 64-token blocks (the tiny config, D = 64)."""
+    monkeypatch.setenv("MOD_ATTN_KERNEL", "dual")
+    L = olayout(w)
+    P = M.Plan(w)
+    q, k, v = syn.family_r(w, seed=709, device="cuda")
+    rng = np.random.default_rng(10)
+    masks = rng.random((1, w.heads, L.n, L.n)) < 0.5
+    masks[0, 0, 1] = False
+    rp, ci = masks_to_csr(masks)
+    o, lse = P.block_sparse_attn_fwd(q, k, v, rp, ci)
+    torch.cuda.synchronize()
+    _check(o, lse, masks, q, k, v, L)
