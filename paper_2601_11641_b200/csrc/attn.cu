@@ -22,7 +22,8 @@
 //               softmax in the log2 domain, bf16 P back into TMEM (tcgen05.st), lazy O rescale only
 //               when the running max grows by > 8 (exact: O_g and l_g share the reference max).
 //               Epilogue: split-KV merge of (m_g, l_g, O_g), O / l -> bf16, lse.
-// TMEM: S[0] [0,BN), S[1] [BN,2BN), O_0 [2BN,2BN+D), O_1 [2BN+D,2BN+2D): 512 (or 256) columns.
+// TMEM: S[b] [b*BN,(b+1)*BN) for b < NS, O_0, O_1 after them: NS = 3 S buffers where they fit
+// (D = 64 or 64-key blocks: the MMA then runs S two blocks ahead of the softmax), else NS = 2.
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
@@ -50,7 +51,13 @@ __device__ __forceinline__ void trace(int dbg, int role, int& cnt, int tag, int 
 template <int D, int BN>
 struct AttnCfg {
   static constexpr int BM = 128;                      // query rows per tile (tcgen05 M)
-  static constexpr int STAGES = 2;                    // K ring slot = j % 2 = S buffer (k_empty == s_full)
+  // S buffers in TMEM: 3 when they fit beside the two O accumulators (D = 64, or 64-key blocks), so the
+  // MMA issues S_{j+2} before PV_j has consumed P_j and each softmax group finds its next S ready
+  // (its MUFU-bound exponentials then run back to back); 2 at D = 128 with 128-key blocks
+  static constexpr int NS = (3 * BN + 2 * D) <= 512 ? 3 : 2;
+  static constexpr int STAGES = NS;                   // K ring slot = j % NS = S buffer (k_empty == s_full)
+  __device__ static int sbuf(int j) { return NS == 2 ? (j & 1) : (int)((unsigned)j % (unsigned)NS); }
+  __device__ static uint32_t sphase(int j) { return NS == 2 ? ((j >> 1) & 1) : (((unsigned)j / (unsigned)NS) & 1u); }
   static constexpr int VSTAGES = 2;                   // V ring slot = j % 2 = O_g (v_empty == o_done[g])
   static constexpr int Q_BOX = BM * 128;              // bytes of one 64-column box of Q
   static constexpr int KV_BOX = BN * 128;             // bytes of one 64-column box of K or V
@@ -61,11 +68,11 @@ struct AttnCfg {
   static constexpr int OFF_K = OFF_Q + Q_BYTES;
   static constexpr int OFF_V = OFF_K + STAGES * KV_BYTES;
   static constexpr int OFF_BAR = OFF_V + VSTAGES * KV_BYTES;
-  static constexpr int NUM_BARS = 1 + STAGES + VSTAGES + 2 + 2 + 2;
+  static constexpr int NUM_BARS = 1 + STAGES + VSTAGES + NS + 2 + 2;
   static constexpr int OFF_RED = OFF_BAR + NUM_BARS * 8 + 16;      // epilogue (m, l) exchange [2][2][128] f32
   static constexpr int SMEM = OFF_RED + 2 * 2 * 128 * 4;
-  static constexpr int TMEM_S0 = 0, TMEM_S1 = BN, TMEM_O = 2 * BN;   // O_g at TMEM_O + g*D
-  static constexpr uint32_t TMEM_COLS = (2 * BN + 2 * D) <= 256 ? 256 : 512;
+  static constexpr int TMEM_O = NS * BN;                            // S[b] at b*BN; O_g at TMEM_O + g*D
+  static constexpr uint32_t TMEM_COLS = (NS * BN + 2 * D) <= 256 ? 256 : 512;
   static constexpr uint32_t IDESC_S = idesc_bf16_f32(BM, BN, false, false);
   static constexpr uint32_t IDESC_O = idesc_bf16_f32(BM, D, false, true);
   static constexpr int THREADS = 320;
@@ -83,8 +90,8 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* q_full = bars;
   uint64_t* k_full = bars + 1;
   uint64_t* v_full = k_full + C::STAGES;
-  uint64_t* s_full = v_full + C::VSTAGES;
-  uint64_t* p_full = s_full + 2;
+  uint64_t* s_full = v_full + C::VSTAGES;   // [NS], per S buffer
+  uint64_t* p_full = s_full + C::NS;
   uint64_t* o_done = p_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
 
@@ -100,8 +107,8 @@ __global__ void __launch_bounds__(320, 1)
     mbar_init(q_full, 1);
     for (int s = 0; s < C::STAGES; ++s) mbar_init(&k_full[s], 1);
     for (int s = 0; s < C::VSTAGES; ++s) mbar_init(&v_full[s], 1);
+    for (int b = 0; b < C::NS; ++b) mbar_init(&s_full[b], 1);
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&s_full[b], 1);
       mbar_init(&p_full[b], 128);
       mbar_init(&o_done[b], 1);
     }
@@ -126,8 +133,8 @@ __global__ void __launch_bounds__(320, 1)
         tma_load_3d(smem + C::OFF_Q + a * C::Q_BOX, &tm_q, q_full, a * 64, qi * block, bh, pol_q);
       int tc_ = 0;
       auto load_k = [&](int j) {
-        const int s = j & 1;
-        if (j >= 2) mbar_wait(&s_full[s], ((j - 2) >> 1) & 1);   // S_{j-2} consumed K slot s
+        const int s = C::sbuf(j);
+        if (j >= C::NS) mbar_wait(&s_full[s], C::NS == 2 ? (((j - 2) >> 1) & 1) : C::sphase(j) ^ 1u);   // S_{j-NS} consumed K slot s
         trace(dbg, 0, tc_, 1, j);
         if (dbg & 2) { mbar_arrive(&k_full[s]); return; }
         unsigned char* dst = smem + C::OFF_K + s * C::KV_BYTES;
@@ -147,10 +154,10 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
         for (int a = 0; a < C::NATOM; ++a) tma_load_3d(dst + a * C::KV_BOX, &tm_v, &v_full[s], a * 64, row, bh, pol_kv);
       };
-      // demand order of the MMA warp: K0, K1, V0, K2, V1, ...
-      load_k(0);
+      // demand order of the MMA warp: K0 .. K_{NS-1}, V0, K_NS, V1, K_{NS+1}, ...
+      for (int j = 0; j < C::NS - 1 && j < L; ++j) load_k(j);
       for (int j = 0; j < L; ++j) {
-        if (j + 1 < L) load_k(j + 1);
+        if (j + C::NS - 1 < L) load_k(j + C::NS - 1);
         load_v(j);
       }
     }
@@ -165,12 +172,12 @@ __global__ void __launch_bounds__(320, 1)
       tc_fence_after();
       int tc_ = 0;
       auto issue_s = [&](int j) {
-        const int b = j & 1;
-        mbar_wait(&k_full[b], (j >> 1) & 1);
+        const int b = C::sbuf(j);
+        mbar_wait(&k_full[b], C::sphase(j));
         trace(dbg, 1, tc_, 10, j);
         tc_fence_after();
         const uint32_t sk = smem_u32(smem + C::OFF_K + b * C::KV_BYTES);
-        const uint32_t d_s = tmem + (b ? C::TMEM_S1 : C::TMEM_S0);
+        const uint32_t d_s = tmem + b * BN;
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           // K-major SW128: 32 bytes per K step inside a 128B atom, atoms one box apart
@@ -181,8 +188,7 @@ __global__ void __launch_bounds__(320, 1)
         mma_commit(&s_full[b]);          // also releases K slot b to the producer
         trace(dbg, 1, tc_, 11, j);
       };
-      issue_s(0);
-      if (L > 1) issue_s(1);
+      for (int j = 0; j < C::NS && j < L; ++j) issue_s(j);
       for (int j = 0; j < L; ++j) {
         const int b = j & 1;
         mbar_wait(&v_full[b], (j >> 1) & 1);
@@ -190,7 +196,7 @@ __global__ void __launch_bounds__(320, 1)
         trace(dbg, 1, tc_, 12, j);
         tc_fence_after();
         const uint32_t sv = smem_u32(smem + C::OFF_V + b * C::KV_BYTES);
-        const uint32_t p_t = tmem + (b ? C::TMEM_S1 : C::TMEM_S0);
+        const uint32_t p_t = tmem + C::sbuf(j) * BN;
 #pragma unroll
         for (int kk = 0; kk < BN / 16; ++kk) {
           // B = V_j: N = D (MN-major, 64-column atoms LBO = KV_BOX apart), K = 16 keys = 2048 bytes
@@ -199,7 +205,7 @@ __global__ void __launch_bounds__(320, 1)
         }
         mma_commit(&o_done[b]);          // also releases V slot b to the producer
         trace(dbg, 1, tc_, 14, j);
-        if (j + 2 < L) issue_s(j + 2);   // S[b] is free once PV_j (issued above, in order) read P_j
+        if (j + C::NS < L) issue_s(j + C::NS);   // S[j % NS] is free once PV_j (issued above, in order) read P_j
       }
     }
   } else {
@@ -208,14 +214,16 @@ __global__ void __launch_bounds__(320, 1)
     const int quarter = warp & 3;          // TMEM lane quarter this warp may access
     const int row = quarter * 32 + lane;   // query row within the tile
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-    const uint32_t t_s = tmem + lane_off + (g ? C::TMEM_S1 : C::TMEM_S0);
     const uint32_t t_og = tmem + lane_off + C::TMEM_O + g * D;
+    const uint32_t t_sg = tmem + lane_off + (g ? BN : 0);   // this group's S buffer when NS == 2
     const int q_row0 = qi * block;
     const int q_rows = min(block, N - q_row0);
     float m_run = -INFINITY, l_run = 0.f;
     int it = 0, tc_ = 0;
     for (int j = g; j < L; j += 2, ++it) {
-      mbar_wait(&s_full[g], it & 1);
+      const int sb = C::NS == 2 ? g : C::sbuf(j);                 // S_j, then P_j
+      const uint32_t t_s = C::NS == 2 ? t_sg : tmem + lane_off + sb * BN;
+      mbar_wait(&s_full[sb], C::NS == 2 ? (uint32_t)(it & 1) : C::sphase(j));
       if (lane == 0 && quarter == 2) trace(dbg, 2 + g, tc_, 20 + g, j);
       tc_fence_after();
       if (dbg & 1) {   // bring-up: MMA/TMA pipeline without the softmax math
