@@ -6,7 +6,7 @@ import numpy as np, torch
 import synthetic as syn, oracle as O
 from gpu_helpers import masks_to_csr, olayout
 import paper_2601_11641_b200 as M
-w = syn.HUNYUAN
+w = syn.CONFIGS[sys.argv[1]] if len(sys.argv) > 1 else syn.HUNYUAN
 L = olayout(w); P = M.Plan(w)
 q, k, v = syn.family_r(w, device="cuda")
 rng = np.random.default_rng(0)
@@ -28,4 +28,4 @@ names = {1: "P:k_empty", 2: "P:v_empty", 10: "M:k_full", 11: "M:S_issued", 12: "
 with open("gpurun_out/trace.txt", "w") as f:
     for t, tag, j in ev:
         f.write(f"{t - t0:9d} {names.get(tag, tag):14s} j={j}\n")
-print("events", n, "span", ev[-1][0] - t0, "list length", int((rp[0, 1000 // L.n, 1000 % L.n + 1] - rp[0, 1000 // L.n, 1000 % L.n]).item()))
+print("events", n, "span", ev[-1][0] - t0, "list length", int((rp[0, 1000 // L.n, 1000 % L.n + 1] - rp[0, 1000 // L.n, 1000 % L.n]).item()), "n", L.n)

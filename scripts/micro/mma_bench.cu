@@ -7,7 +7,7 @@ using namespace sm100;
 template <int N, bool TS, int MODE = 0>   // MODE 0: B K-major; 1: B MN-major (like V); 2: S(SS,K-major) + PV(TS,MN-major) alternating;
 // 3: 8 MMAs + commit; 4: 8 MMAs + commit + wait on a completed barrier; 5: 8 MMAs + wait (no commit);
 // 6: SS MMAs while warps 1-3 stream tcgen05.ld/st over other TMEM columns (softmax-like traffic); 7: same with TS MMAs
-__global__ void __launch_bounds__(128, 1) k(long long* cyc, int niter) {
+__global__ void __launch_bounds__(288, 1) k(long long* cyc, int niter) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ uint32_t slot;
@@ -51,6 +51,28 @@ __global__ void __launch_bounds__(128, 1) k(long long* cyc, int niter) {
     }
     if (acc == 0x12345678u) cyc[0] = acc;
   }
+  if ((MODE == 16 || MODE == 17) && threadIdx.x >= 32) {
+    // warps 1..8: softmax-like TMEM traffic on their lane quarter: ld 128 columns of S, st 64 of P
+    const int w = threadIdx.x / 32;
+    const uint32_t base = tmem + ((uint32_t)((w & 3) * 32) << 16) + ((w >> 2) & 1) * 128;
+    uint32_t r[4][32];
+    uint32_t acc = 0;
+    while (!stop_flag) {
+      tmem_ld32(base, r[0]);
+      tmem_ld32(base + 32, r[1]);
+      tmem_ld32(base + 64, r[2]);
+      tmem_ld32(base + 96, r[3]);
+      tmem_ld_wait();
+      acc += r[0][0] + r[1][5] + r[2][9] + r[3][31];
+      if (MODE == 17) {
+        tmem_st32(base, r[0]);
+        tmem_st32(base + 32, r[1]);
+        tmem_st_wait();
+      }
+      for (int d = 0; d < 40; ++d) acc = acc * 1664525u + 1013904223u;   // some ALU work between bursts
+    }
+    if (acc == 0x12345678u) cyc[0] = acc;
+  }
   if ((MODE == 6 || MODE == 7) && threadIdx.x >= 32) {
     // warps 1-3: lane quarters 1-3, columns [256, 384): ld 32 columns, st them back, repeat
     const int w = threadIdx.x / 32;
@@ -72,7 +94,7 @@ __global__ void __launch_bounds__(128, 1) k(long long* cyc, int niter) {
     const uint32_t sa = smem_u32(smem), sb = smem_u32(smem + 32768);  // B: up to 256 rows x 2 atoms = 64KB
     long long t0 = clock64();
     for (int it = 0; it < niter; ++it) {
-      if (MODE >= 12) {
+      if (MODE >= 12) {  // 16/17: as 12 with softmax-like TMEM traffic from 8 warps
         // K4's tensor-pipe sequence per block pair (j even / odd share nothing but the pipe):
         //   PV_j: A = P_j (bf16, TMEM S[b]), D = O_b;  S_{j+2}: D = S[b] (overwrites what PV_j read).
         // 12: exactly that (WAR on S[b] right after PV_j);  13: S_{j+2} into a disjoint region (no WAR);
@@ -148,10 +170,11 @@ template <int N, bool TS, int MODE = 0> void run(const char* name) {
   auto kern = k<N, TS, MODE>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024 + 1024);
   int niter = 2000;
-  kern<<<148, 128, 160 * 1024 + 1024>>>(d, niter);
+  const int nthr = (MODE == 16 || MODE == 17) ? 288 : 128;
+  kern<<<148, nthr, 160 * 1024 + 1024>>>(d, niter);
   printf("first launch %s\n", cudaGetErrorString(cudaDeviceSynchronize())); fflush(stdout);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  cudaEventRecord(e0); kern<<<148, 128, 160 * 1024 + 1024>>>(d, niter); cudaEventRecord(e1); cudaEventSynchronize(e1);
+  cudaEventRecord(e0); kern<<<148, nthr, 160 * 1024 + 1024>>>(d, niter); cudaEventRecord(e1); cudaEventSynchronize(e1);
   float ms; cudaEventElapsedTime(&ms, e0, e1);
   long long h[148]; cudaMemcpy(h, d, 148 * 8, cudaMemcpyDeviceToHost);
   double avg = 0; for (int i = 0; i < 148; ++i) avg += h[i]; avg /= 148;
@@ -181,5 +204,7 @@ int main() {
   run<128, false, 13>("K4seq noWAR");
   run<128, false, 14>("K4seq+sync");
   run<128, false, 15>("K4seq+commit");
+  run<128, false, 16>("K4seq+8w ld");
+  run<128, false, 17>("K4seq+8w ld/st");
   return 0;
 }
