@@ -254,7 +254,7 @@ def run_ours(args):
     def step(timed_kernels=False):
         if seq is not None:
             for dst, src in zip((q, k, v), seq):
-                dst.copy_(seq_to_heads(src))
+                seq_to_heads(src, out=dst)
         if timed_kernels:
             e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
             e[0].record(stream)
@@ -274,7 +274,7 @@ def run_ours(args):
             P.collect_block_stats(q, k, out=Wf)
         P.update_online_mask(Wf, rp, ci, hist, xs_prev, xs_curr)
         if seq is not None:
-            step.o_seq = heads_to_seq(o)
+            step.o_seq = heads_to_seq(o, out=step.o_seq if getattr(step, "o_seq", None) is not None else None)
         if timed_kernels:
             e[3].record(stream)
             ev["attn"].append((e[1], e[2]))

@@ -221,6 +221,27 @@ mod_status mod_linearity_nre(mod_plan plan, const double* x_prev, const double* 
 /* Dense mask helper (the warm-up's full attention, Alg. 1): all-ones CSR. */
 mod_status mod_fill_dense_mask(mod_plan plan, int32_t* row_ptr, int32_t* col_idx, void* stream);
 
+/* ---- Ulysses relayout around the sequence<->head all-to-all (BASELINE config 5) ----
+ * When activations arrive sequence-sharded over P ranks, the per-head hot path ("We process
+ * each attention head independently") needs head shards; the exchange is an all-to-all of contiguous
+ * per-peer chunks (NCCL all_to_all_single).  These four calls are the pack before it and the unpack
+ * after it, both directions.  All tensors are DEVICE bf16, contiguous, 16-byte aligned; src and dst
+ * must not alias; head_dim D in {64, 128}.  Stream-ordered, asynchronous.  Errors: NULL pointer ->
+ * MOD_ERR_USAGE; non-divisible sizes, bad D, aliasing or misalignment -> MOD_ERR_INPUT.
+ *   seq_pack:    x_seq [B,Ns,H,D]      -> send [P,B,Ns,H/P,D]     (chunk p = heads [p*H/P, (p+1)*H/P))
+ *   seq_unpack:  recv [P,B,Ns,Hp,D]    -> x_head [B,Hp,P*Ns,D]    (chunk p = tokens [p*Ns, (p+1)*Ns))
+ *   head_pack:   x_head [B,Hp,N,D]     -> send [P,B,N/P,Hp,D]     (chunk p = tokens [p*N/P, (p+1)*N/P))
+ *   head_unpack: recv [P,B,Ns,Hp,D]    -> x_seq [B,Ns,P*Hp,D]     (chunk p = heads [p*Hp, (p+1)*Hp))
+ * With P = 1 each pack/unpack is the [B,N,H,D] <-> [B,H,N,D] transpose. */
+mod_status mod_ulysses_seq_pack(const void* x_seq, void* send, int32_t B, int32_t Ns, int32_t H, int32_t D,
+                                int32_t P, void* stream);
+mod_status mod_ulysses_seq_unpack(const void* recv, void* x_head, int32_t B, int32_t Ns, int32_t Hp, int32_t D,
+                                  int32_t P, void* stream);
+mod_status mod_ulysses_head_pack(const void* x_head, void* send, int32_t B, int32_t N, int32_t Hp, int32_t D,
+                                 int32_t P, void* stream);
+mod_status mod_ulysses_head_unpack(const void* recv, void* x_seq, int32_t B, int32_t Ns, int32_t Hp, int32_t D,
+                                   int32_t P, void* stream);
+
 /* Number of kernels the last successful compute call on this thread launched (for bench.py). */
 int32_t mod_last_launch_count(void);
 

@@ -70,6 +70,10 @@ SIGNATURES = {
     "mod_map_rel_error": (I32, [P, P, P, P, P, P]),
     "mod_linearity_nre": (I32, [P, P, P, I32, I32, P, C.POINTER(I32), I32, P, P]),
     "mod_last_launch_count": (I32, []),
+    "mod_ulysses_seq_pack": (I32, [P, P, I32, I32, I32, I32, I32, P]),
+    "mod_ulysses_seq_unpack": (I32, [P, P, I32, I32, I32, I32, I32, P]),
+    "mod_ulysses_head_pack": (I32, [P, P, I32, I32, I32, I32, I32, P]),
+    "mod_ulysses_head_unpack": (I32, [P, P, I32, I32, I32, I32, I32, P]),
 }
 
 

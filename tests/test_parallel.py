@@ -18,6 +18,32 @@ def _free_port():
     return p
 
 
+class TorchRelayout:
+    """Test-side reference of the pack / unpack maps (include/moddit.h mod_ulysses_*), in torch, so
+    that the all-to-all plumbing runs on CPU with gloo.  The CUDA kernels are pinned to the same maps
+    in tests/test_gpu_ulysses.py."""
+
+    @staticmethod
+    def seq_pack(x_seq, P):
+        B, Ns, H, D = x_seq.shape
+        return x_seq.reshape(B, Ns, P, H // P, D).permute(2, 0, 1, 3, 4).contiguous()
+
+    @staticmethod
+    def seq_unpack(recv):
+        P, B, Ns, Hp, D = recv.shape
+        return recv.permute(1, 3, 0, 2, 4).reshape(B, Hp, P * Ns, D).contiguous()
+
+    @staticmethod
+    def head_pack(x_head, P):
+        B, Hp, N, D = x_head.shape
+        return x_head.reshape(B, Hp, P, N // P, D).permute(2, 0, 3, 1, 4).contiguous()
+
+    @staticmethod
+    def head_unpack(recv):
+        P, B, Ns, Hp, D = recv.shape
+        return recv.permute(1, 2, 0, 3, 4).reshape(B, Ns, P * Hp, D).contiguous()
+
+
 def _worker(rank, ws, port, B, N, H, D, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -27,11 +53,11 @@ def _worker(rank, ws, port, B, N, H, D, q):
         full = torch.randn((B, N, H, D), generator=g)         # [B, N, H, D] activations, identical on all ranks
         Ns = N // ws
         x_seq = full[:, rank * Ns:(rank + 1) * Ns].contiguous()
-        x_head = seq_to_heads(x_seq)
+        x_head = seq_to_heads(x_seq, relayout=TorchRelayout)
         h0, h1 = head_range(H, ws, rank)
         ref = full.permute(0, 2, 1, 3)[:, h0:h1].contiguous()  # [B, H/P, N, D]
         ok1 = torch.equal(x_head, ref)
-        back = heads_to_seq(x_head)
+        back = heads_to_seq(x_head, relayout=TorchRelayout)
         ok2 = torch.equal(back, x_seq)
         q.put((rank, ok1, ok2))
     finally:
@@ -61,3 +87,10 @@ def test_head_range_and_lpt():
     assert sorted(sum(parts, [])) == list(range(6))
     loads = [sum([5, 1, 4, 2, 3, 3][h] for h in p) for p in parts]
     assert max(loads) - min(loads) <= 1
+
+
+def test_relayout_reference_maps_p1():
+    """At P = 1 the maps are the [B,N,H,D] <-> [B,H,N,D] transpose (what seq_to_heads returns)."""
+    x = torch.randn(2, 5, 6, 8)
+    assert torch.equal(seq_to_heads(x, relayout=TorchRelayout), x.permute(0, 2, 1, 3))
+    assert torch.equal(heads_to_seq(x.permute(0, 2, 1, 3).contiguous(), relayout=TorchRelayout), x)
