@@ -16,7 +16,7 @@ themselves are marked "parity unpinned" below and in DESIGN.md:
     (block mean of token scores, rows sum to 1, closed form for constant blocks).
 """
 from .layout import Layout, make_layout  # noqa: F401
-from .stats import (pooled_block_stats, exact_sparsity, exact_sparsity_masked, sparsity_from_map,  # noqa: F401
+from .stats import (pooled_block_stats, exact_sparsity, exact_sparsity_masked, exact_sparsity_masked_rows, sparsity_from_map,  # noqa: F401
                     informativeness_from_sparsity)  # noqa: F401
 from .fit import (basis_C, basis_D, basis_E, design_matrix, gram_closed_form, gram_materialized,  # noqa: F401
                   rhs, rhs_materialized, solve_normal, fit_mixture, nae, reconstruct_from_x)

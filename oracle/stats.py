@@ -114,3 +114,32 @@ def exact_sparsity_masked(q, k, masks, L: Layout, eta: float = 1e-4, scale: floa
                     jlo, jhi = L.block_range(j)
                     S[b, h, i, j] = (P[ilo:ihi, jlo:jhi] < eta).sum() / ((ihi - ilo) * (jhi - jlo))
     return S, lse
+
+
+def exact_sparsity_masked_rows(q, k, mask, L: Layout, b: int, h: int, qblocks, eta: float = 1e-4,
+                               scale: float | None = None):
+    """exact_sparsity_masked for the query blocks ``qblocks`` of one (b, h) only (the same Eq. 2 on the
+    masked, renormalised map, row block by row block), so that full-size layouts can be checked on
+    samples.  ``mask`` is that head's n x n block mask.  Returns {i: (S_row [n] with NaN off the mask,
+    lse [|I_i|])}."""
+    q = _f64(q)[b, h]
+    k = _f64(k)[b, h]
+    mask = np.asarray(mask, dtype=bool)
+    s = 1.0 / np.sqrt(L.head_dim) if not scale else float(scale)
+    N = q.shape[0]
+    tb = np.arange(N) // L.block
+    out = {}
+    for i in qblocks:
+        ilo, ihi = L.block_range(i)
+        A = s * q[ilo:ihi] @ k.T
+        A = np.where(mask[i][tb][None, :], A, -np.inf)
+        m = A.max(axis=1, keepdims=True)
+        e = np.exp(A - m)
+        z = e.sum(axis=1, keepdims=True)
+        P = e / z
+        row = np.full(L.n, np.nan)
+        for j in np.nonzero(mask[i])[0]:
+            jlo, jhi = L.block_range(j)
+            row[j] = (P[:, jlo:jhi] < eta).sum() / ((ihi - ilo) * (jhi - jlo))
+        out[int(i)] = (row, (m + np.log(z))[:, 0])
+    return out

@@ -407,3 +407,54 @@ def test_exact_sparsity_with_kernel_lse(M):
     S_m, _ = O.exact_sparsity_masked(q.cpu(), k.cpu(), masks, L, 1e-4)
     d = np.abs((1 - U.double().cpu().numpy()[masks]) - S_m[masks])
     assert d.max() <= 0.02 and d.mean() <= 1e-3      # K4 lse error (<= 5e-3) moves a few threshold decisions
+
+
+# ------------------------------------------------------------------------------------------ full-size samples
+def test_update_parity_hunyuan_sampled_heads(M):
+    """K3 at the Hunyuan 720p layout (n = 929, p = 2819): Eq. 5 merge bit-level, refit vs the oracle."""
+    w = syn.HUNYUAN.with_heads(2)
+    L = olayout(w)
+    P = plan_for(M, w)
+    Wf = syn.random_stats(w.batch, w.heads, L.n, seed=81, device="cuda")
+    hist = syn.random_stats(w.batch, w.heads, L.n, seed=82, device="cuda")
+    masks = _structured_masks(L, w.heads, 83, top_k=164)
+    rp, ci = masks_to_csr(masks)
+    xp = syn.random_intensities(w.batch, w.heads, L.p, seed=84, device="cuda")
+    xc = syn.random_intensities(w.batch, w.heads, L.p, seed=85, device="cuda")
+    hist0, xc0 = hist.cpu().numpy().copy(), xc.cpu().numpy().copy()
+    P.update_online_mask(Wf, rp, ci, hist, xp, xc)
+    torch.cuda.synchronize()
+    ref_hist = O.reconstruct_history(Wf.double().cpu().numpy(), hist0.astype(np.float64), masks, True)
+    hg = hist.cpu().numpy()
+    assert np.array_equal(hg[~masks], hist0[~masks])
+    ulp = np.spacing(np.abs(ref_hist[masks]).astype(np.float32))
+    assert np.all(np.abs(hg[masks].astype(np.float64) - ref_hist[masks]) <= ulp)
+    assert np.array_equal(xp.cpu().numpy(), xc0)
+    xr = O.fit_mixture(hg.astype(np.float64), L)
+    _check_x(xc.cpu().numpy(), xr, L, np.linalg.cond(O.gram_closed_form(L)))
+
+
+def test_exact_sparsity_hunyuan_sampled_rows(M):
+    """f1 EXACT statistic at the Hunyuan 720p layout with K4's own lse, on sampled query blocks."""
+    w = syn.HUNYUAN.with_heads(1)
+    L = olayout(w)
+    P = plan_for(M, w)
+    q, k, v = syn.family_s(w, device="cuda")
+    masks = _structured_masks(L, 1, 86, top_k=164)
+    rp, ci = masks_to_csr(masks)
+    _, lse = P.block_sparse_attn_fwd(q, k, v, rp, ci)
+    U = P.collect_exact_sparsity(q, k, lse, rp, ci, 1e-4)
+    torch.cuda.synchronize()
+    Un = U.double().cpu().numpy()[0, 0]
+    assert np.all(np.isnan(Un[~masks[0, 0]]))
+    rng = np.random.default_rng(87)
+    counts = masks[0, 0].sum(1)
+    blocks = sorted({0, L.n - 1, int(np.argmax(counts)), int(rng.integers(0, L.n))})
+    rows = O.exact_sparsity_masked_rows(q.cpu(), k.cpu(), masks[0, 0], L, 0, 0, blocks, 1e-4)
+    for i, (row, lse_ref) in rows.items():
+        lo, hi = L.block_range(i)
+        assert np.abs(lse[0, 0, lo:hi].double().cpu().numpy() - lse_ref).max() <= 5e-3
+        sel = ~np.isnan(row)
+        d = np.abs((1.0 - Un[i][sel]) - row[sel])
+        # K4's lse (<= 5e-3) and fp32 dot products move the few probabilities that sit at eta
+        assert d.max() <= 0.02 and d.mean() <= 2e-3, (i, d.max(), d.mean())

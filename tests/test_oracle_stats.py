@@ -105,3 +105,21 @@ def test_masked_exact_sparsity_renormalises_over_selection():
     Sm, _ = O.exact_sparsity_masked(q, k, m, L, 1e-9)
     assert np.all(np.isnan(Sm[0, 0, :, 1:]))
     assert np.all(Sm[0, 0, :, 0] == 0.0)     # no probability over a single 4-key block falls below 1e-9
+
+
+def test_masked_exact_sparsity_rows_match_the_whole_map():
+    """The row-sampled form (used for full-size GPU checks) restricts the same Eq. 2 computation."""
+    L = _lay()
+    rng = np.random.default_rng(6)
+    q = rng.standard_normal((1, 2, L.N, 8)) * 1.5
+    k = rng.standard_normal((1, 2, L.N, 8)) * 1.5
+    m = rng.random((1, 2, L.n, L.n)) < 0.5
+    m[0, 1, 2] = True
+    Sm, lse = O.exact_sparsity_masked(q, k, m, L, 1e-2)
+    rows = O.exact_sparsity_masked_rows(q, k, m[0, 1], L, 0, 1, range(L.n), 1e-2)
+    for i, (row, lse_i) in rows.items():
+        lo, hi = L.block_range(i)
+        assert np.array_equal(np.isnan(row), np.isnan(Sm[0, 1, i]))
+        assert np.allclose(row[~np.isnan(row)], Sm[0, 1, i][~np.isnan(row)], atol=0)
+        if m[0, 1, i].any():
+            assert np.allclose(lse_i, lse[0, 1, lo:hi], atol=1e-12)
