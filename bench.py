@@ -518,7 +518,7 @@ def main():
     ap.add_argument("--sparsity", type=float, default=0.878)
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-chunks", type=int, default=8, help="head chunks of the pipelined e2e leg")
+    ap.add_argument("--e2e-chunks", type=int, default=24, help="head chunks of the pipelined e2e leg")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-blocks", type=int, default=4)
