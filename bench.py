@@ -102,14 +102,25 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------------------- distributed
+# MOD_BENCH_DIST_BACKEND=gloo (bring-up only): run the N>1 code path with gloo for the scalar
+# reductions, several ranks sharing the visible GPUs -- validates the multi-rank logic on a 1-GPU box
+# (the timings of such a run mean nothing).  The default, and every measured run, is NCCL.
+DIST_BACKEND = os.environ.get("MOD_BENCH_DIST_BACKEND", "nccl")
+
+
 def dist_setup(n_gpus: int):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if ws > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if DIST_BACKEND == "gloo":
+            local = local % torch.cuda.device_count()
+            torch.cuda.set_device(local)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     else:
         torch.cuda.set_device(0)
     return ws, rank, local
@@ -125,7 +136,7 @@ def max_over_ranks(x: float, ws: int) -> float:
     if ws == 1:
         return x
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device="cpu" if DIST_BACKEND == "gloo" else "cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -134,7 +145,7 @@ def sum_over_ranks(x: float, ws: int) -> float:
     if ws == 1:
         return x
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device="cpu" if DIST_BACKEND == "gloo" else "cuda")
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
 
