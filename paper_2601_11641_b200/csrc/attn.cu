@@ -28,6 +28,7 @@
 
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -47,6 +48,16 @@ __device__ __forceinline__ void trace(int dbg, int role, int& cnt, int tag, int 
     ++cnt;
   }
 }
+
+template <int I, int N, typename F>
+__device__ __forceinline__ void static_for_impl(F&& f) {
+  if constexpr (I < N) {
+    f(std::integral_constant<int, I>{});
+    static_for_impl<I + 1, N>(f);
+  }
+}
+template <int N, typename F>
+__device__ __forceinline__ void static_for(F&& f) { static_for_impl<0, N>(f); }
 
 template <int D, int BN>
 struct AttnCfg {
@@ -171,41 +182,50 @@ __global__ void __launch_bounds__(320, 1)
       mbar_wait(q_full, 0);
       tc_fence_after();
       int tc_ = 0;
-      auto issue_s = [&](int j) {
-        const int b = C::sbuf(j);
+      auto issue_s = [&](int j, int b) {   // b = C::sbuf(j) (a literal where the caller knows it)
         mbar_wait(&k_full[b], C::sphase(j));
         trace(dbg, 1, tc_, 10, j);
         tc_fence_after();
-        const uint32_t sk = smem_u32(smem + C::OFF_K + b * C::KV_BYTES);
+        const uint64_t a_base = smem_desc_sw128(sq, 16, 1024);
+        const uint64_t b_base = smem_desc_sw128(smem_u32(smem + C::OFF_K + b * C::KV_BYTES), 16, 1024);
         const uint32_t d_s = tmem + b * BN;
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          // K-major SW128: 32 bytes per K step inside a 128B atom, atoms one box apart
-          const uint64_t ad = smem_desc_sw128(sq + (kk / 4) * C::Q_BOX + (kk % 4) * 32, 16, 1024);
-          const uint64_t bd = smem_desc_sw128(sk + (kk / 4) * C::KV_BOX + (kk % 4) * 32, 16, 1024);
-          mma_ss(d_s, ad, bd, C::IDESC_S, kk > 0 ? 1u : 0u);
-        }
+        // K-major SW128: 32 bytes per K step inside a 128B atom, atoms one box apart (offsets in 16 B)
+        static_for<D / 16>([&](auto kc) {
+          constexpr int kk = decltype(kc)::value;
+          mma_ss_off<((kk / 4) * C::Q_BOX + (kk % 4) * 32) / 16, ((kk / 4) * C::KV_BOX + (kk % 4) * 32) / 16>(
+              d_s, a_base, b_base, C::IDESC_S, kk > 0 ? 1u : 0u);
+        });
         mma_commit(&s_full[b]);          // also releases K slot b to the producer
         trace(dbg, 1, tc_, 11, j);
       };
-      for (int j = 0; j < C::NS && j < L; ++j) issue_s(j);
-      for (int j = 0; j < L; ++j) {
-        const int b = j & 1;
+      for (int j = 0; j < C::NS && j < L; ++j) issue_s(j, C::sbuf(j));
+      // PV_j, then S_{j+NS} into the S buffer PV_j just read
+      auto pv_then_s = [&](int j, int b, int sb) {
         mbar_wait(&v_full[b], (j >> 1) & 1);
         mbar_wait(&p_full[b], (j >> 1) & 1);
         trace(dbg, 1, tc_, 12, j);
         tc_fence_after();
-        const uint32_t sv = smem_u32(smem + C::OFF_V + b * C::KV_BYTES);
-        const uint32_t p_t = tmem + C::sbuf(j) * BN;
-#pragma unroll
-        for (int kk = 0; kk < BN / 16; ++kk) {
-          // B = V_j: N = D (MN-major, 64-column atoms LBO = KV_BOX apart), K = 16 keys = 2048 bytes
-          const uint64_t bd = smem_desc_sw128(sv + kk * 2048, C::KV_BOX, 1024);
-          mma_ts(tmem + C::TMEM_O + b * D, p_t + kk * 8, bd, C::IDESC_O, (j > 1 || kk > 0) ? 1u : 0u);
-        }
+        const uint64_t v_base = smem_desc_sw128(smem_u32(smem + C::OFF_V + b * C::KV_BYTES), C::KV_BOX, 1024);
+        const uint32_t p_t = tmem + sb * BN;
+        const uint32_t acc0 = j > 1 ? 1u : 0u;
+        // B = V_j: N = D (MN-major, 64-column atoms LBO = KV_BOX apart), K = 16 keys = 2048 bytes
+        static_for<BN / 16>([&](auto kc) {
+          constexpr int kk = decltype(kc)::value;
+          mma_ts_off<kk * 8, kk * 2048 / 16>(tmem + C::TMEM_O + b * D, p_t, v_base, C::IDESC_O, kk > 0 ? 1u : acc0);
+        });
         mma_commit(&o_done[b]);          // also releases V slot b to the producer
         trace(dbg, 1, tc_, 14, j);
-        if (j + C::NS < L) issue_s(j + C::NS);   // S[j % NS] is free once PV_j (issued above, in order) read P_j
+        if (j + C::NS < L) issue_s(j + C::NS, sb);   // S[sb] is free once PV_j (issued above, in order) read P_j
+      };
+      if constexpr (C::NS == 2) {
+        // unrolled by two so that every slot index is a compile-time constant: the descriptors and
+        // TMEM addresses of both halves are loop-invariant (uniform registers, no per-MMA R2UR)
+        for (int j = 0; j < L; j += 2) {
+          pv_then_s(j, 0, 0);
+          if (j + 1 < L) pv_then_s(j + 1, 1, 1);
+        }
+      } else {
+        for (int j = 0; j < L; ++j) pv_then_s(j, j & 1, C::sbuf(j));
       }
     }
   } else {

@@ -117,6 +117,32 @@ __device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// Same MMAs with the descriptors formed inside the asm as base + compile-time offset (in 16-byte
+// units), so that only the two loop-invariant bases stay live and ptxas can keep them uniform.
+template <uint32_t A_OFF, uint32_t B_OFF>
+__device__ __forceinline__ void mma_ss_off(uint32_t d_tmem, uint64_t a_base, uint64_t b_base, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\n.reg .b64 ad, bd;\n"
+      "add.s64 ad, %1, %5;\n"
+      "add.s64 bd, %2, %6;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], ad, bd, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a_base), "l"(b_base), "r"(idesc), "r"(accumulate), "n"((uint64_t)A_OFF), "n"((uint64_t)B_OFF)
+      : "memory");
+}
+template <uint32_t A_COL, uint32_t B_OFF>
+__device__ __forceinline__ void mma_ts_off(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_base, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\n.reg .b64 bd;\n.reg .b32 at;\n"
+      "add.s32 at, %1, %5;\n"
+      "add.s64 bd, %2, %6;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [at], bd, %3, p;\n}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_base), "r"(idesc), "r"(accumulate), "n"(A_COL), "n"((uint64_t)B_OFF)
+      : "memory");
+}
 // D[tmem] (+)= A[smem] * B[smem]^T, kind::i8 (signed int8 in, int32 accumulate)
 __device__ __forceinline__ void mma_ss_i8(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                           uint32_t accumulate) {
