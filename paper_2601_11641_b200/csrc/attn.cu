@@ -49,16 +49,6 @@ __device__ __forceinline__ void trace(int dbg, int role, int& cnt, int tag, int 
   }
 }
 
-template <int I, int N, typename F>
-__device__ __forceinline__ void static_for_impl(F&& f) {
-  if constexpr (I < N) {
-    f(std::integral_constant<int, I>{});
-    static_for_impl<I + 1, N>(f);
-  }
-}
-template <int N, typename F>
-__device__ __forceinline__ void static_for(F&& f) { static_for_impl<0, N>(f); }
-
 template <int D, int BN>
 struct AttnCfg {
   static constexpr int BM = 128;                      // query rows per tile (tcgen05 M)

@@ -5,6 +5,7 @@
 // layout type [61,64) with SWIZZLE_128B = 2; instruction descriptor for kind::f16: D fmt [4,6),
 // A fmt [7,10), B fmt [10,13), A/B major [15], [16], N>>3 [17,23), M>>4 [24,29)).
 #pragma once
+#include <type_traits>
 #include <cuda.h>
 #include <stdint.h>
 
@@ -143,6 +144,16 @@ __device__ __forceinline__ void mma_ts_off(uint32_t d_tmem, uint32_t a_tmem, uin
       "r"(a_tmem), "l"(b_base), "r"(idesc), "r"(accumulate), "n"(A_COL), "n"((uint64_t)B_OFF)
       : "memory");
 }
+template <int I, int N, typename F>
+__device__ __forceinline__ void static_for_impl(F&& f) {
+  if constexpr (I < N) {
+    f(std::integral_constant<int, I>{});
+    static_for_impl<I + 1, N>(f);
+  }
+}
+template <int N, typename F>
+__device__ __forceinline__ void static_for(F&& f) { static_for_impl<0, N>(f); }   // f(integral_constant<int, i>)
+
 // D[tmem] (+)= A[smem] * B[smem]^T, kind::i8 (signed int8 in, int32 accumulate)
 __device__ __forceinline__ void mma_ss_i8(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                           uint32_t accumulate) {
