@@ -354,7 +354,10 @@ def run_ours(args):
         pipelined = not (q8 or exact or seq is not None) and w.batch == 1
         if pipelined:
             from paper_2601_11641_b200.pipeline import HeadChunkPipeline
-            chunks = max(c for c in range(1, min(args.e2e_chunks, Hl) + 1) if Hl % c == 0)
+            want = args.e2e_chunks
+            if want <= 0:   # auto: ~80 MB of upload per chunk (24 chunks at Hunyuan 720p, 4 at CogVideoX)
+                want = max(1, round(3 * q.numel() * 2 / (80 << 20)))
+            chunks = max(c for c in range(1, min(want, Hl) + 1) if Hl % c == 0)
             pipe = HeadChunkPipeline(w, chunks, top_k=1, tau_e=0.0, masked_renorm=True)
 
             def chunk_step(plan, c, qc, kc, vc, oc):
@@ -529,7 +532,8 @@ def main():
     ap.add_argument("--sparsity", type=float, default=0.878)
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-chunks", type=int, default=24, help="head chunks of the pipelined e2e leg")
+    ap.add_argument("--e2e-chunks", type=int, default=0,
+                    help="head chunks of the pipelined e2e leg (0: about 80 MB of upload per chunk)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-blocks", type=int, default=4)
