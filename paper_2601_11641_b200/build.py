@@ -47,6 +47,8 @@ def _stale() -> bool:
 
 def build_library(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
+        if any(not os.path.exists(src[:-2]) for src in glob.glob(os.path.join(ROOT, "examples", "*.c"))):
+            build_examples()
         return LIB
     os.makedirs(BUILD, exist_ok=True)
     cc = nvcc()
@@ -70,7 +72,25 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     os.replace(tmp, LIB)
+    build_examples()
     return LIB
+
+
+EXAMPLES = os.path.join(ROOT, "examples")
+
+
+def build_examples() -> list[str]:
+    """Plain-C consumers of the C ABI (examples/*.c), linked against the in-tree libmoddit.so."""
+    out = []
+    for src in sorted(glob.glob(os.path.join(EXAMPLES, "*.c"))):
+        exe = src[:-2]
+        cmd = [nvcc(), "-x", "cu", *ARCH, "-O2", "-I", INCLUDE, "-o", exe, src, "-L", PKG, "-lmoddit",
+               "-Xlinker", "-rpath,$ORIGIN/../paper_2601_11641_b200"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"example build failed for {src}:\n{r.stdout}\n{r.stderr}")
+        out.append(exe)
+    return out
 
 
 if __name__ == "__main__":

@@ -53,3 +53,16 @@ def test_version_and_error_string_without_gpu():
     st = m.lib.mod_plan_create(ctypes.byref(ModLayout(1, 1, 96, 0, 1, 1, 1, 128)),
                                ctypes.byref(ModConfig(1e-8, 0.0, 1, 0, 0.0, 0, 1, 1, 0.0)), 0, ctypes.byref(h))
     assert st == 2 and b"head_dim=96" in m.lib.mod_last_error()
+
+
+def test_plain_c_example_links_against_the_library():
+    """examples/moddit_step.c drives the hot path through moddit.h alone (no Python); it must build
+    and resolve libmoddit.so from the tree (the GPU run is tests/test_gpu_c_example.py)."""
+    from paper_2601_11641_b200.build import build_examples
+    exe = os.path.join(ROOT, "examples", "moddit_step")
+    if not os.path.exists(exe):
+        build_examples()
+    out = subprocess.run(["ldd", exe], capture_output=True, text=True).stdout
+    assert re.search(r"libmoddit\.so => .*paper_2601_11641_b200/libmoddit\.so", out), out
+    usage = subprocess.run([exe], capture_output=True, text=True)
+    assert usage.returncode == 1 and "usage" in usage.stderr
