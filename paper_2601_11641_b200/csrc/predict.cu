@@ -5,8 +5,8 @@
 //     intensities, evaluated in IEEE fp64 without contraction so that the integer decisions below
 //     match the oracle bit for bit:  d = x_c - x_p;  s = d / (t_c - t_p);  x_hat = x_c + s*(t - t_c);
 //  2. selection over the 3n-1 pool (§5.3; reading Z3: keys descending, Z14: ties by id):
-//     TOPK / TOPMASS sort the (key, id) pairs with an in-shared-memory bitonic network; THRESHOLD
-//     compares directly.  TOPMASS accumulates max(key,0)*|supp| sequentially in sorted order;
+//     TOPK takes the K-th largest key by a radix select (no sort); TOPMASS sorts the (key, id)
+//     pairs with an in-shared-memory bitonic network; THRESHOLD compares directly.  TOPMASS accumulates max(key,0)*|supp| sequentially in sorted order;
 //  3. block mask = selected diagonals (j - i = delta_k) | selected columns | kept frame squares
 //     [a_r,b_r]^2 | diagonal guard | prefix rows/columns (Alg. 1; Z15, Z17),
 //     emitted as a CSR index list.  Steps 1 (one CTA per head), 2 (row counts) and 3 (row
@@ -18,6 +18,68 @@ namespace {
 
 __device__ __forceinline__ bool before(double ka, int ia, double kb, int ib) {
   return ka > kb || (ka == kb && ia < ib);
+}
+
+
+// Order-preserving map of a double to uint64 (larger key -> larger code; -0 folded onto +0 so that
+// equal keys compare equal, as in the oracle's numeric comparison).
+__device__ __forceinline__ unsigned long long key_code(double x) {
+  unsigned long long b = (unsigned long long)__double_as_longlong(x == 0.0 ? 0.0 : x);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// Radix select, one CTA: the k-th largest (k >= 1) of the values code(e) over the elements e < P for
+// which pred(e) holds, BITS wide, 8 bits per pass from the top.  Returns the value; `hist` is a
+// 256-int shared buffer.  All threads must call it.
+template <int BITS, typename Code, typename Pred>
+__device__ unsigned long long radix_kth_largest(int P, int k, Code code, Pred pred, int* hist) {
+  __shared__ unsigned long long s_prefix;
+  __shared__ int s_k;
+  const int t = threadIdx.x;
+  unsigned long long prefix = 0, mask = 0;
+  for (int shift = BITS - 8; shift >= 0; shift -= 8) {
+    for (int b = t; b < 256; b += blockDim.x) hist[b] = 0;
+    __syncthreads();
+    for (int e = t; e < P; e += blockDim.x) {
+      if (!pred(e)) continue;
+      const unsigned long long c = code(e);
+      if ((c & mask) == prefix) atomicAdd(&hist[(c >> shift) & 255], 1);
+    }
+    __syncthreads();
+    if (t < 32) {
+      // lane l owns bins [255 - 8l - 7, 255 - 8l] (from the top); warp scan of the lane sums
+      int own = 0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) own += hist[255 - 8 * t - u];
+      int incl = own;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (t >= o) incl += y;
+      }
+      const int excl = incl - own;
+      const unsigned hit = __ballot_sync(0xffffffffu, incl >= k && excl < k);
+      const int lane = __ffs(hit) - 1;
+      if (t == lane) {
+        int cum = excl;
+        for (int u = 0; u < 8; ++u) {
+          const int bin = 255 - 8 * t - u;
+          if (cum + hist[bin] >= k) {
+            s_prefix = prefix | ((unsigned long long)bin << shift);
+            s_k = k - cum;
+            break;
+          }
+          cum += hist[bin];
+        }
+      }
+    }
+    __syncthreads();
+    prefix = s_prefix;
+    k = s_k;
+    mask |= 255ull << shift;
+    __syncthreads();
+  }
+  return prefix;
 }
 
 struct PredictArgs {
@@ -63,6 +125,37 @@ __global__ void __launch_bounds__(1024) select_kernel(PredictArgs a) {
   __syncthreads();
   if (a.mode == MOD_SELECT_THRESHOLD) {
     for (int e = t; e < P; e += blockDim.x) sel[e] = keys[e] > a.param;
+    return;
+  }
+  if (a.mode == MOD_SELECT_TOPK && P <= 0xffff) {
+    // Top-K by radix select instead of a full sort: T = the K-th largest key code; every key above T
+    // is in, and of the keys equal to T the lowest ids fill the remaining places (reading Z14: key
+    // descending, ties by ascending pattern id) -- the same set the sorted order gives.
+    __shared__ int hist[256];
+    __shared__ int n_above;
+    const int K = min(a.top_k, P);
+    if (K >= P) {
+      for (int e = t; e < P; e += blockDim.x) sel[e] = 1;
+      return;
+    }
+    const unsigned long long T = radix_kth_largest<64>(
+        P, K, [&](int e) { return key_code(keys[e]); }, [](int) { return true; }, hist);
+    if (t == 0) n_above = 0;
+    __syncthreads();
+    int mine = 0;
+    for (int e = t; e < P; e += blockDim.x) mine += key_code(keys[e]) > T;
+    mine = __reduce_add_sync(0xffffffffu, mine);
+    if ((t & 31) == 0) atomicAdd(&n_above, mine);
+    __syncthreads();
+    const int m = K - n_above;   // >= 1 places for keys equal to T, lowest ids first
+    const unsigned long long id_code = radix_kth_largest<16>(
+        P, m, [&](int e) { return (unsigned long long)(0xffff - e); },
+        [&](int e) { return key_code(keys[e]) == T; }, hist);
+    const int max_id = 0xffff - (int)id_code;
+    for (int e = t; e < P; e += blockDim.x) {
+      const unsigned long long c = key_code(keys[e]);
+      sel[e] = c > T || (c == T && e <= max_id);
+    }
     return;
   }
   for (int k = 2; k <= P2; k <<= 1) {

@@ -154,6 +154,25 @@ def test_predict_bit_exact_given_x(M, w, mode, param):
     assert np.array_equal(rp[..., -1].cpu().numpy(), ref.sum((-1, -2)))
 
 
+@pytest.mark.parametrize("w", [SMALL_PREFIX, syn.HUNYUAN.with_heads(2)], ids=lambda w: w.name)
+@pytest.mark.parametrize("K", [1, 7, 100, 10 ** 6])
+def test_predict_topk_ties_bit_exact(M, w, K):
+    """Top-K with massive exact ties, signed zeros and negative keys (reading Z14: ties by ascending
+    pattern id): the GPU's radix select must pick the oracle's set."""
+    L = olayout(w)
+    P = plan_for(M, w, top_k=K)
+    g = torch.Generator().manual_seed(91)
+    # intensities on a coarse grid of 5 values (incl. 0 and -0) -> keys repeat across many patterns
+    vals = torch.tensor([-1.0, -0.0, 0.0, 0.5, 2.0], dtype=torch.float64)
+    xc = vals[torch.randint(0, 5, (w.batch, w.heads, L.p), generator=g)].cuda()
+    xp = xc.clone()                      # x_hat = x_curr exactly (zero slope)
+    rp, ci = P.predict_block_mask(xp, xc, 11, 12, 13, None)
+    torch.cuda.synchronize()
+    ref = O.predict_block_mask(xp.cpu().numpy(), xc.cpu().numpy(), 11, 12, 13,
+                               np.zeros((w.batch, w.heads, w.frames)), L, O.SELECT_TOPK, K, 0.0, True)
+    assert np.array_equal(csr_to_masks(rp, ci, L.n), ref)
+
+
 def test_predict_without_keep_and_guard(M):
     w = SMALL_PREFIX
     L = olayout(w)
