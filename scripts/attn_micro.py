@@ -3,23 +3,19 @@ MOD_ATTN_DEBUG=1: softmax skipped (MMA+TMA only); =2: K/V TMA skipped; =3 both."
 import os, sys, json, subprocess
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
-import synthetic as syn, oracle as O
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
-from gpu_helpers import masks_to_csr, olayout
+import synthetic as syn
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from _masks import structured_csr
 import paper_2601_11641_b200 as M
 from bench import attn_flops
 
 w = syn.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "hunyuanvideo-720p"]
-L = olayout(w)
 P = M.Plan(w)
 q, k, v = syn.family_r(w, device="cuda")
-rng = np.random.default_rng(0)
-masks = np.zeros((1, w.heads, L.n, L.n), dtype=bool)
-for h in range(w.heads):
-    sel = O.select_patterns(rng.standard_normal(3 * L.n - 1), L.n, O.SELECT_TOPK, max(4, L.n // 12))
-    masks[0, h] = O.block_mask(sel, rng.random(L.frames) < 0.7, L, True)
-rp, ci = masks_to_csr(masks)
-fl = attn_flops(rp.cpu().numpy(), ci.cpu().numpy(), L.N, L.block, L.head_dim)
+rp, ci = structured_csr(P, w)
+nnz = float(rp[..., -1].sum().item())
+density = nnz / (w.batch * w.heads * P.n * P.n)
+fl = attn_flops(rp.cpu().numpy(), ci.cpu().numpy(), w.tokens, w.block, w.head_dim)
 o, lse = P.block_sparse_attn_fwd(q, k, v, rp, ci)
 torch.cuda.synchronize()
 import threading, pynvml
@@ -36,7 +32,7 @@ for _ in range(REPS):
 e1.record(); torch.cuda.synchronize(); stop.set(); th.join()
 ms = e0.elapsed_time(e1) / REPS
 mhz = float(np.median(clk)) if clk else float("nan")
-nnz = float(masks.sum()); iters_per_sm = nnz / 148
+iters_per_sm = nnz / 148
 print(json.dumps({"lib": os.environ.get("MODDIT_LIB_OVERRIDE", "default"), "dbg": os.environ.get("MOD_ATTN_DEBUG", "0"),
-                  "density": round(float(masks.mean()), 4), "ms": round(ms, 3), "tflops": round(fl / ms / 1e9, 1),
+                  "density": round(density, 4), "ms": round(ms, 3), "tflops": round(fl / ms / 1e9, 1),
                   "sm_mhz": mhz, "watts": round(float(np.median(pw[len(pw)//3:])), 0) if pw else None, "mhz_late": float(np.median(clk[len(clk)//3:])) if clk else None, "cycles_per_block_iter": round(ms * 1e-3 * mhz * 1e6 / iters_per_sm, 1)}))

@@ -1,20 +1,17 @@
 """Dump the clock64 event trace of CTA 1000 (MOD_ATTN_DEBUG=16|x) at the Hunyuan shape."""
 import ctypes, os, sys, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
 import numpy as np, torch
-import synthetic as syn, oracle as O
-from gpu_helpers import masks_to_csr, olayout
+import synthetic as syn
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from _masks import structured_csr
 import paper_2601_11641_b200 as M
 w = syn.CONFIGS[sys.argv[1]] if len(sys.argv) > 1 else syn.HUNYUAN
-L = olayout(w); P = M.Plan(w)
+P = M.Plan(w)
 q, k, v = syn.family_r(w, device="cuda")
-rng = np.random.default_rng(0)
-masks = np.zeros((1, w.heads, L.n, L.n), dtype=bool)
-for h in range(w.heads):
-    sel = O.select_patterns(rng.standard_normal(3 * L.n - 1), L.n, O.SELECT_TOPK, max(4, L.n // 12))
-    masks[0, h] = O.block_mask(sel, rng.random(L.frames) < 0.7, L, True)
-rp, ci = masks_to_csr(masks)
+rp, ci = structured_csr(P, w)
+nnz = float(rp[..., -1].sum().item())
+density = nnz / (w.batch * w.heads * P.n * P.n)
 o, lse = P.block_sparse_attn_fwd(q, k, v, rp, ci); torch.cuda.synchronize()
 buf = (ctypes.c_longlong * (5 * 4096 * 2))()
 M.lib.mod_debug_attn_trace(buf, 5 * 4096 * 2)
@@ -28,4 +25,4 @@ names = {1: "P:k_empty", 2: "P:v_empty", 10: "M:k_full", 11: "M:S_issued", 12: "
 with open("gpurun_out/trace.txt", "w") as f:
     for t, tag, j in ev:
         f.write(f"{t - t0:9d} {names.get(tag, tag):14s} j={j}\n")
-print("events", n, "span", ev[-1][0] - t0, "list length", int((rp[0, 1000 // L.n, 1000 % L.n + 1] - rp[0, 1000 // L.n, 1000 % L.n]).item()), "n", L.n)
+print("events", n, "span", ev[-1][0] - t0, "list length", int((rp[0, 1000 // P.n, 1000 % P.n + 1] - rp[0, 1000 // P.n, 1000 % P.n]).item()), "n", P.n)

@@ -1,31 +1,27 @@
 """Quantized (INT8 QK / FP8 PV) vs bf16 K4 at a config's shape with structured masks."""
 import os, sys, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
 import numpy as np, torch
-import synthetic as syn, oracle as O
-from gpu_helpers import masks_to_csr, olayout
+import synthetic as syn
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from _masks import structured_csr
 import paper_2601_11641_b200 as M
 from bench import attn_flops
 
 w = syn.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "hunyuanvideo-720p"]
 REPS = int(os.environ.get("REPS", "10"))
-L = olayout(w)
 P = M.Plan(w)
 q, k, v = syn.family_s(w, step=12, device="cuda")
-rng = np.random.default_rng(0)
-masks = np.zeros((1, w.heads, L.n, L.n), dtype=bool)
-for h in range(w.heads):
-    sel = O.select_patterns(rng.standard_normal(3 * L.n - 1), L.n, O.SELECT_TOPK, max(4, L.n // 12))
-    masks[0, h] = O.block_mask(sel, rng.random(L.frames) < 0.7, L, True)
-rp, ci = masks_to_csr(masks)
-fl = attn_flops(rp.cpu().numpy(), ci.cpu().numpy(), L.N, L.block, L.head_dim)
+rp, ci = structured_csr(P, w)
+nnz = float(rp[..., -1].sum().item())
+density = nnz / (w.batch * w.heads * P.n * P.n)
+fl = attn_flops(rp.cpu().numpy(), ci.cpu().numpy(), w.tokens, w.block, w.head_dim)
 qb = P.quantize_qkv(q, k, v)
 o8, l8 = P.block_sparse_attn_fwd_q8(qb, rp, ci)
 ob, lb = P.block_sparse_attn_fwd(q, k, v, rp, ci)
 torch.cuda.synchronize()
 d = (o8.float() - ob.float()).abs()
-res = {"config": w.name, "density": round(float(masks.mean()), 4), "tflop": round(fl / 1e12, 3),
+res = {"config": w.name, "density": round(density, 4), "tflop": round(fl / 1e12, 3),
        "q8_vs_bf16_max_abs": round(d.max().item(), 4), "q8_vs_bf16_mean_abs": round(d.mean().item(), 6),
        "lse_max_abs": round((l8 - lb).abs().max().item(), 5)}
 def t(fn):
