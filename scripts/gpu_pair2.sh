@@ -1,5 +1,13 @@
+# CTA-pair K4 (MOD_ATTN_KERNEL=pair2) vs the default kernel: bench step at Hunyuan / Wan, dense mode
 mkdir -p gpurun_out
-timeout 300 python -m pytest tests/test_gpu_attn_pair.py -q -x --timeout 120 > gpurun_out/pytest_pair.log 2>&1; echo pair_rc=$?; tail -2 gpurun_out/pytest_pair.log
-MOD_ATTN_KERNEL=pair MOD_ATTN_DEBUG=16 python scripts/attn_trace.py 2>&1 | grep -v Warn | tail -1; cp gpurun_out/trace.txt gpurun_out/trace_pair.txt
-for rep in 1 2; do for kk in single pair; do MOD_ATTN_KERNEL=$kk timeout 100 python scripts/attn_micro.py 2>&1 | grep '^{' | sed "s/^/$kk /"; done; done
-for kk in single pair; do MOD_ATTN_KERNEL=$kk REPS=300 timeout 200 python scripts/attn_micro.py 2>&1 | grep '^{' | sed "s/^/sustained $kk /"; done
+for c in hunyuanvideo-720p wan2.1-14b-720p; do for kk in single pair2 single pair2; do
+MOD_ATTN_KERNEL=$kk timeout 300 python bench.py --config $c --steps 10 --warmup 3 --no-dense --no-e2e --no-cpu > gpurun_out/bp2.log 2>&1
+python - <<PY
+import json
+for l in open('gpurun_out/bp2.log'):
+    if l.startswith('{'):
+        d=json.loads(l); print('$c', '$kk', {k:d[k] for k in ('value','attn_ms','attn_tflops')}, d['clocks']['sm_mhz'])
+    elif 'rror' in l: print(l[:200])
+PY
+done; done
+for kk in single pair2; do MOD_ATTN_KERNEL=$kk HEADS=8 timeout 120 python scripts/attn_dense_time.py 2>&1 | grep "^{" | sed "s/^/dense $kk /" | cut -c1-200; done

@@ -1,6 +1,7 @@
 """K4 kernel variants against the fp64 oracle: the one-block-per-CTA kernel (default), the
-paired-query-block kernel (MOD_ATTN_KERNEL=pair) and the two-CTAs-per-SM
-single-chain kernel (MOD_ATTN_KERNEL=dual).
+paired-query-block kernel (MOD_ATTN_KERNEL=pair), the two-CTAs-per-SM
+single-chain kernel (MOD_ATTN_KERNEL=dual) and the CTA-pair kernel with M = 256 cta_group::2 MMAs over
+the union of two rows' lists (MOD_ATTN_KERNEL=pair2; D = 128 only, other shapes fall back).
 
 The pair kernel walks the merged index list of query blocks 2p and 2p+1 and shares each K/V tile
 between them, so its masks are chosen to exercise every shape of that merge: lists that coincide,
@@ -30,7 +31,7 @@ def M():
     return m
 
 
-@pytest.fixture(params=["pair", "single", "dual"])
+@pytest.fixture(params=["pair", "single", "dual", "pair2"])
 def kernel(request, monkeypatch):
     monkeypatch.setenv("MOD_ATTN_KERNEL", request.param)
     return request.param
