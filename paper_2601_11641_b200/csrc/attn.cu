@@ -1012,7 +1012,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
       mbar_init(&k_full[s], 1);
       mbar_init(&v_full[s], 1);
       mbar_init(&s_full[s], 1);
-      mbar_init(&p_full[s], 256);   // 128 softmax threads of each CTA
+      mbar_init(&p_full[s], 8);     // one elected lane per softmax warp, 4 warps in each CTA
       mbar_init(&o_done[s], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1179,7 +1179,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
       }
       tmem_st_wait();
       tc_fence_before();
-      mbar_arrive_cluster(p_full_leader);
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(p_full_leader);   // one (remote) arrival per warp
     }
     // epilogue: merge the two split-KV partials of this CTA's row block
     auto red = reinterpret_cast<float(*)[2][128]>(smem + C::OFF_RED);
