@@ -207,7 +207,7 @@ def run_ours(args):
     burst, sustained, hbm, peak_src = load_peaks()
 
     exact = args.stat == "exact"
-    P = Plan(w, top_k=1, tau_e=0.0, masked_renorm=not exact)
+    P = Plan(w, top_k=1, tau_e=0.0, masked_renorm=not exact, attn_kernel=args.attn_kernel)
     gen = dict(seed=syn.SEED_BASE, device="cuda", head_offset=h0, total_heads=w_full.heads)
     extra = {}
 
@@ -358,7 +358,7 @@ def run_ours(args):
             if want <= 0:   # auto: ~80 MB of upload per chunk (24 chunks at Hunyuan 720p, 4 at CogVideoX)
                 want = max(1, round(3 * q.numel() * 2 / (80 << 20)))
             chunks = max(c for c in range(1, min(want, Hl) + 1) if Hl % c == 0)
-            pipe = HeadChunkPipeline(w, chunks, top_k=1, tau_e=0.0, masked_renorm=True)
+            pipe = HeadChunkPipeline(w, chunks, top_k=1, tau_e=0.0, masked_renorm=True, attn_kernel=args.attn_kernel)
 
             def chunk_step(plan, c, qc, kc, vc, oc):
                 hs = pipe.heads(c)
@@ -397,11 +397,17 @@ def run_ours(args):
         del hq, hk, hv, ho
 
     # ---- roofline of the dominant kernel (K4): algorithmic FLOPs / event-timed launch duration
-    traffic = None
+    # traffic: DRAM bytes per launch from the committed ncu --set full capture of this kernel on this
+    # config (profiles/k4_traffic.json), scaled to this rank's heads (each head's bytes are independent)
+    traffic, traffic_src = None, None
+    kname = P.attn_kernel_name()
     tp = os.path.join(ROOT, "profiles", "k4_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(args.config)
+            rec = json.load(open(tp)).get(args.config)
+            if rec and rec.get("kernel") == kname:
+                traffic = round(rec["bytes"] * Hl / rec["heads"])
+                traffic_src = f"{rec['source']}; x {Hl}/{rec['heads']} heads"
         except Exception:
             traffic = None
     # the quantized kernel's peak: the measured bf16 figure x the guide's nominal 2x ratio for 8-bit MMAs
@@ -409,8 +415,8 @@ def run_ours(args):
     roof = {"bound": "tensor", "achieved": round(attn_tflops, 1), "peak": pk, "unit": "TFLOP/s",
             "frac": round(attn_tflops / pk, 4), "frac_of_sustained": round(attn_tflops / (sustained * (2 if q8 else 1)), 4),
             "peak_source": peak_src + (" (bf16 x 2, nominal 8-bit ratio)" if q8 else ""),
-            "traffic": None if q8 else traffic,
-            "kernel": "quantize (3 kernels) + attn_q8_kernel" if q8 else "attn_fwd_kernel<128,128>",
+            "traffic": None if q8 else traffic, "traffic_source": None if q8 else traffic_src,
+            "kernel": "quantize (3 kernels) + attn_q8_kernel" if q8 else kname,
             "algorithmic_flops_per_launch": flops_local}
 
     out.update({
@@ -433,7 +439,7 @@ def run_ours(args):
 
     # ---- cpu baseline: the oracle as it stands on a bounded sample (rank 0, N=1 only)
     if rank == 0 and ws == 1 and not args.no_cpu:
-        out["cpu_baseline"] = cpu_baseline(w, q, k, v, rpn, cin, args.cpu_seconds)
+        out["cpu_baseline"] = cpu_baseline(w, q, k, v, rpn, cin, args.cpu_seconds, x_prev0, x_curr0, keep, K)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if ws > 1:
@@ -441,28 +447,70 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def cpu_baseline(w, q, k, v, rpn, cin, budget_s: float):
-    """Oracle masked attention on sampled query blocks of head 0 (same mask), timed on host cores."""
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def cpu_baseline(w, q, k, v, rpn, cin, budget_s: float, x_prev0=None, x_curr0=None, keep=None, K=None, Wf=None):
+    """The oracle as it stands, timed on the host cores, rank 0 at N = 1:
+    * the mask pipeline of one head at full n^2 scale, timed in full: pooled statistic (O2), fit (O4,
+      Cholesky of the p x p Gram), predict + select + mask (O6-O8) and the Eq. 5 update + refit (O10);
+    * masked attention (O9) on sampled query blocks of head 0 under the bench's own mask (its TFLOPS is
+      the line's ``value``), and the full-shape attention time EXTRAPOLATED from the sample by the
+      selected-block count of all heads."""
     import oracle as O
     L = O.make_layout(1, 1, w.head_dim, w.prefix_tokens, w.frames, w.height, w.width, w.block)
     mask = O.csr_to_mask(rpn[0, 0], cin[0, 0], L.n)
     qh, kh, vh = (t[:, :1].cpu() for t in (q, k, v))
+    pipe = {}
+    t0 = time.perf_counter()
+    W = O.pooled_block_stats(qh, kh, L)
+    pipe["stats_s"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    X = O.fit_mixture(W, L)
+    pipe["fit_s"] = time.perf_counter() - t0
+    if x_prev0 is not None:
+        xp = x_prev0[:, :1].double().cpu().numpy()
+        xc = x_curr0[:, :1].double().cpu().numpy()
+        kp = keep[:, :1].cpu().numpy()
+        t0 = time.perf_counter()
+        O.predict_block_mask(xp, xc, M_WARMUP - 1, M_WARMUP, M_WARMUP + DT, kp, L, O.SELECT_TOPK, K)
+        pipe["predict_s"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        hist = O.reconstruct_history(W, W.copy(), mask[None, None], True)
+        O.fit_mixture(hist, L)
+        pipe["update_s"] = time.perf_counter() - t0
+    del X
     rng = np.random.default_rng(0)
     order = rng.permutation(L.n)
     t0 = time.perf_counter()
-    flops, nb = 0.0, 0
+    flops, nb, blocks_done = 0.0, 0, 0
     for i in order:
         O.masked_attention_rows(qh, kh, vh, mask, L, 0, 0, [int(i)])
         lo, hi = L.block_range(int(i))
         keys = sum(L.block_size(j) for j in np.nonzero(mask[i])[0])
         flops += 4.0 * w.head_dim * (hi - lo) * keys
+        blocks_done += int(mask[i].sum())
         nb += 1
         if time.perf_counter() - t0 > budget_s:
             break
     dt = time.perf_counter() - t0
+    total_blocks = float(rpn[..., -1].sum())
     return {"value": flops / dt / 1e12, "unit": "TFLOPS", "cores": os.cpu_count(), "kind": "oracle",
-            "sample": f"{nb} query blocks of head 0 (oracle masked_attention_rows, fp64 numpy, same mask), "
-                      f"{dt:.1f} s", "threads": torch.get_num_threads()}
+            "cpu_model": _cpu_model(), "threads": torch.get_num_threads(),
+            "sample": f"{nb} query blocks of head 0 (oracle masked_attention_rows, fp64 numpy, the bench's mask), "
+                      f"{dt:.1f} s; mask pipeline of head 0 at full n^2 scale timed in full",
+            "pipeline_one_head_s": {k_: round(v_, 3) for k_, v_ in pipe.items()},
+            "attention_full_shape_s_extrapolated": round(dt / max(blocks_done, 1) * total_blocks, 1),
+            "extrapolation": "sampled seconds per selected block x selected blocks of all heads (labelled, not run)"}
 
 
 # ---------------------------------------------------------------------------------------- reference arm
@@ -522,6 +570,18 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
+def _self_launch(n: int) -> None:
+    """`python bench.py --gpus N` without a launcher: re-exec under torch.distributed.run with N ranks
+    (one process per GPU, rendezvous on 127.0.0.1) and exit with its status."""
+    import socket
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    raise SystemExit(subprocess.call(cmd))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -542,9 +602,16 @@ def main():
     ap.add_argument("--stat", default="pooled", choices=["pooled", "exact"],
                     help="block statistic: pooled (north_star (1)) or the paper's exact Eq. 2 (SURVEY f1)")
     ap.add_argument("--eta", type=float, default=1e-4)
+    ap.add_argument("--attn-kernel", default="default", choices=["default", "splitkv", "pair", "pair2"],
+                    help="K4 schedule (include/moddit.h mod_attn_kernel); default is the headline kernel")
     ap.add_argument("--ulysses", action="store_true",
                     help="sequence-sharded inputs: Ulysses all-to-all in and out of every step (config 5)")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        _self_launch(args.gpus)
+    ws_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws_env != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws_env}: launch one rank per GPU")
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.impl == "reference":

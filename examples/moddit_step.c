@@ -58,7 +58,7 @@ int main(int argc, char** argv) {
   L.height = atoi(argv[6]);
   L.width = atoi(argv[7]);
   L.block = atoi(argv[8]);
-  mod_config cfg = {1e-8, 0.0f, atoi(argv[9]), MOD_SELECT_TOPK, 0.0f, MOD_STAT_POOLED, 1, 1, 0.0f};
+  mod_config cfg = {1e-8, 0.0f, atoi(argv[9]), MOD_SELECT_TOPK, 0.0f, MOD_STAT_POOLED, 1, 1, 0.0f, MOD_ATTN_DEFAULT};
 
   mod_plan plan;
   CHECK(mod_plan_create(&L, &cfg, 0, &plan));

@@ -70,6 +70,15 @@ typedef enum {
   MOD_STAT_POOLED = 0       /* north_star (1): mean-pooled q.k block score + row softmax mass */
 } mod_stat_mode;
 
+/* K4 kernel schedule (all compute the same Eq. 1 result; parity-tested alike).  DEFAULT is the one
+ * bench.py times; the others are kept for A/B measurement. */
+typedef enum {
+  MOD_ATTN_DEFAULT = 0,     /* one 8-warp softmax group over column halves, NS S buffers ahead of it */
+  MOD_ATTN_SPLITKV = 1,     /* two 4-warp softmax groups splitting the index list (round-1 kernel) */
+  MOD_ATTN_PAIR = 2,        /* two query blocks per CTA walking their merged index list (f4) */
+  MOD_ATTN_PAIR2 = 3        /* CTA pair, cta_group::2 M = 256 MMAs over two rows' lists (f4; D = 128) */
+} mod_attn_kernel;
+
 typedef struct {
   int32_t batch, heads, head_dim;  /* B, H, D; D in {64, 128} */
   int32_t prefix_tokens;           /* P0 >= 0 (226 for CogVideoX text tokens) */
@@ -87,6 +96,7 @@ typedef struct {
   int32_t masked_renorm;/* 1: Eq. 5 uses the fresh map renormalised over the selected blocks (Z12) */
   int32_t diag_guard;   /* 1: every row keeps block (i,i) (reading Z15) */
   float softmax_scale;  /* 0 -> 1/sqrt(D) */
+  int32_t attn_kernel;  /* mod_attn_kernel (K4 schedule); 0 = default */
 } mod_config;
 
 /* Per-call selection override for mod_predict_block_mask (nullable: plan defaults). */
@@ -121,6 +131,9 @@ mod_status mod_plan_diagnostics(mod_plan plan, double* min_pivot, int32_t* null_
 const double* mod_plan_gram_inverse(mod_plan plan);
 const char* mod_last_error(void);
 const char* mod_version(void);
+/* Name of the K4 kernel instantiation mod_block_sparse_attn_fwd launches for this plan (static string,
+ * e.g. "attn_fwd_kernel<128,128>"), so that measurements can name what they timed. */
+const char* mod_attn_kernel_name(mod_plan plan);
 
 /* K1: W[b,h,i,j] = |I_j| exp(z_ij) / sum_j' |I_j'| exp(z_ij'),  z_ij = s * qbar_i . kbar_j,
  * qbar_i = mean_{p in I_i} Q_p (fp32 accumulation), s = softmax_scale.
@@ -159,7 +172,7 @@ mod_status mod_block_sparse_attn_fwd(mod_plan plan, const void* q, const void* k
                                      void* ws, void* stream);
 
 /* EXACT statistic (Eq. 2) in informativeness polarity (reading Z3):
- * for every block (i,j) listed in the CSR, stats[b,h,i,j] = 1 - S_ij with
+ * for every block (i,j) listed in the CSR, stats[b,h,i,j] = -S_ij with
  *   S_ij = #{(p,q) in I_i x I_j : exp(s Q_p.K_q - lse_p) < eta} / (|I_i||I_j|)   (strict <),
  * lse: fp32 [B,H,N] natural-log row normalisers -- from mod_block_sparse_attn_fwd on the dense list
  * (warm-up, full map) or on the sparse list (Eq. 5's A_masked renormalised over the kept blocks).

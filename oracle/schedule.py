@@ -37,7 +37,7 @@ class OracleSchedule:
         if self.stat == "pooled":
             return pooled_block_stats(q, k, self.L)
         S, _ = exact_sparsity_masked(q, k, mask, self.L, self.eta)     # Eq. 2 on (masked) P; NaN off-mask
-        return 1.0 - S                                                 # reading Z3
+        return -S                                                      # reading Z3
 
     def step(self, t, q, k, v, mask_override=None, compute_attention=True):
         L = self.L

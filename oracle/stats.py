@@ -3,7 +3,8 @@
 O2' EXACT (§4.1 Eq. 2): S_(i,j) = (1/B^2) sum_{x,y} 1(A_(iB+x, jB+y) < eta),
    with A the post-softmax attention map (reading Z2, Alg. 1 P:995 "A = softmax(QK^T/sqrt d)"),
    strict "<", eta = 1e-4 (App. A).  Ragged blocks divide by |I_i||I_j| (Z16).
-   Informativeness polarity (reading Z3): U = 1 - S ("less S = more informative").
+   Informativeness polarity (reading Z3): U = -S ("less S = more informative"), so that the
+   paper's ascending Top-K on fit(S) is the descending Top-K on fit(U) = -fit(S) exactly.
 
 O2 POOLED (BASELINE.json north_star (1); the hot-path substitute for Eq. 2, reading Z1):
    qbar_i = mean_{p in I_i} Q_p, kbar_j likewise; z_ij = s * qbar_i . kbar_j, s = 1/sqrt(D)
@@ -80,8 +81,9 @@ def sparsity_from_map(A, L: Layout, eta: float = 1e-4):
 
 
 def informativeness_from_sparsity(S):
-    """Reading Z3: U = 1 - S (larger = more informative)."""
-    return 1.0 - np.asarray(S, dtype=np.float64)
+    """Reading Z3: U = -S (larger = more informative; fit(U) = -fit(S), so descending on fit(U) is the
+    paper's ascending-on-fit(S) Top-K of P:437 with no per-family offset)."""
+    return -np.asarray(S, dtype=np.float64)
 
 
 def exact_sparsity_masked(q, k, masks, L: Layout, eta: float = 1e-4, scale: float | None = None):

@@ -16,6 +16,8 @@ STATUS_NAMES = {0: "MOD_OK", 1: "MOD_ERR_USAGE", 2: "MOD_ERR_INPUT", 3: "MOD_ERR
                 5: "MOD_ERR_UNSUPPORTED"}
 MOD_SELECT_TOPK, MOD_SELECT_THRESHOLD, MOD_SELECT_TOPMASS = 0, 1, 2
 MOD_STAT_POOLED = 0
+MOD_ATTN_DEFAULT, MOD_ATTN_SPLITKV, MOD_ATTN_PAIR, MOD_ATTN_PAIR2 = range(4)
+ATTN_KERNELS = {"default": MOD_ATTN_DEFAULT, "splitkv": MOD_ATTN_SPLITKV, "pair": MOD_ATTN_PAIR, "pair2": MOD_ATTN_PAIR2}
 
 
 class ModLayout(C.Structure):
@@ -27,7 +29,8 @@ class ModLayout(C.Structure):
 class ModConfig(C.Structure):
     _fields_ = [("lambda_", C.c_double), ("tau_e", C.c_float), ("top_k", C.c_int32),
                 ("select_mode", C.c_int32), ("select_param", C.c_float), ("stat_mode", C.c_int32),
-                ("masked_renorm", C.c_int32), ("diag_guard", C.c_int32), ("softmax_scale", C.c_float)]
+                ("masked_renorm", C.c_int32), ("diag_guard", C.c_int32), ("softmax_scale", C.c_float),
+                ("attn_kernel", C.c_int32)]
 
 
 class ModSelection(C.Structure):
@@ -55,6 +58,7 @@ SIGNATURES = {
     "mod_plan_gram_inverse": (P, [P]),
     "mod_last_error": (C.c_char_p, []),
     "mod_version": (C.c_char_p, []),
+    "mod_attn_kernel_name": (C.c_char_p, [P]),
     "mod_collect_block_stats": (I32, [P, P, P, P, P, P]),
     "mod_fit_mixture": (I32, [P, P, P, P, P, P]),
     "mod_keep_frames": (I32, [P, P, P, P, P]),

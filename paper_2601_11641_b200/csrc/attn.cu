@@ -38,19 +38,9 @@ using namespace sm100;
 namespace {
 
 constexpr int kEmuPairsPer8 = 2;
-// bring-up tracing (MOD_ATTN_DEBUG bit 16): clock64 stamps of one CTA's pipeline events
-constexpr int kTraceCap = 4096;               // events per role
-__device__ long long g_trace[5][kTraceCap][2];  // role: 0 producer, 1 S issuer, 2/3 softmax g0/g1, 4 PV issuer
-__device__ __forceinline__ void trace(int dbg, int role, int& cnt, int tag, int j) {
-  if ((dbg & 16) && blockIdx.x == 1000 && cnt < kTraceCap) {
-    g_trace[role][cnt][0] = clock64();
-    g_trace[role][cnt][1] = ((long long)tag << 32) | (unsigned)j;
-    ++cnt;
-  }
-}
 
 template <int D, int BN>
-struct AttnCfg {
+struct SplitCfg {
   static constexpr int BM = 128;                      // query rows per tile (tcgen05 M)
   // S buffers in TMEM: 3 when they fit beside the two O accumulators (D = 64, or 64-key blocks), so the
   // MMA issues S_{j+2} before PV_j has consumed P_j and each softmax group finds its next S ready
@@ -81,11 +71,11 @@ struct AttnCfg {
 
 template <int D, int BN>
 __global__ void __launch_bounds__(320, 1)
-    attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+    attn_split_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const int* __restrict__ row_ptr,
                     const int* __restrict__ col_idx, __nv_bfloat16* __restrict__ out, float* __restrict__ lse,
-                    int N, int n, int block, float scale_log2, int dbg) {
-  using C = AttnCfg<D, BN>;
+                    int N, int n, int block, float scale_log2) {
+  using C = SplitCfg<D, BN>;
   extern __shared__ __align__(1024) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* q_full = bars;
@@ -132,12 +122,9 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
       for (int a = 0; a < C::NATOM; ++a)
         tma_load_3d(smem + C::OFF_Q + a * C::Q_BOX, &tm_q, q_full, a * 64, qi * block, bh, pol_q);
-      int tc_ = 0;
       auto load_k = [&](int j) {
         const int s = C::sbuf(j);
         if (j >= C::NS) mbar_wait(&s_full[s], C::NS == 2 ? (((j - 2) >> 1) & 1) : C::sphase(j) ^ 1u);   // S_{j-NS} consumed K slot s
-        trace(dbg, 0, tc_, 1, j);
-        if (dbg & 2) { mbar_arrive(&k_full[s]); return; }
         unsigned char* dst = smem + C::OFF_K + s * C::KV_BYTES;
         mbar_arrive_expect_tx(&k_full[s], C::KV_BYTES);
         const int row = cols[j] * block;
@@ -147,8 +134,6 @@ __global__ void __launch_bounds__(320, 1)
       auto load_v = [&](int j) {
         const int s = j & 1;
         if (j >= 2) mbar_wait(&o_done[s], ((j - 2) >> 1) & 1);   // PV_{j-2} consumed V slot s
-        trace(dbg, 0, tc_, 2, j);
-        if (dbg & 2) { mbar_arrive(&v_full[s]); return; }
         unsigned char* dst = smem + C::OFF_V + s * C::KV_BYTES;
         mbar_arrive_expect_tx(&v_full[s], C::KV_BYTES);
         const int row = cols[j] * block;
@@ -171,10 +156,8 @@ __global__ void __launch_bounds__(320, 1)
       const uint32_t sq = smem_u32(smem + C::OFF_Q);
       mbar_wait(q_full, 0);
       tc_fence_after();
-      int tc_ = 0;
       auto issue_s = [&](int j, int b) {   // b = C::sbuf(j) (a literal where the caller knows it)
         mbar_wait(&k_full[b], C::sphase(j));
-        trace(dbg, 1, tc_, 10, j);
         tc_fence_after();
         const uint64_t a_base = smem_desc_sw128(sq, 16, 1024);
         const uint64_t b_base = smem_desc_sw128(smem_u32(smem + C::OFF_K + b * C::KV_BYTES), 16, 1024);
@@ -186,14 +169,12 @@ __global__ void __launch_bounds__(320, 1)
               d_s, a_base, b_base, C::IDESC_S, kk > 0 ? 1u : 0u);
         });
         mma_commit(&s_full[b]);          // also releases K slot b to the producer
-        trace(dbg, 1, tc_, 11, j);
       };
       for (int j = 0; j < C::NS && j < L; ++j) issue_s(j, C::sbuf(j));
       // PV_j, then S_{j+NS} into the S buffer PV_j just read
       auto pv_then_s = [&](int j, int b, int sb) {
         mbar_wait(&v_full[b], (j >> 1) & 1);
         mbar_wait(&p_full[b], (j >> 1) & 1);
-        trace(dbg, 1, tc_, 12, j);
         tc_fence_after();
         const uint64_t v_base = smem_desc_sw128(smem_u32(smem + C::OFF_V + b * C::KV_BYTES), C::KV_BOX, 1024);
         const uint32_t p_t = tmem + sb * BN;
@@ -204,7 +185,6 @@ __global__ void __launch_bounds__(320, 1)
           mma_ts_off<kk * 8, kk * 2048 / 16>(tmem + C::TMEM_O + b * D, p_t, v_base, C::IDESC_O, kk > 0 ? 1u : acc0);
         });
         mma_commit(&o_done[b]);          // also releases V slot b to the producer
-        trace(dbg, 1, tc_, 14, j);
         if (j + C::NS < L) issue_s(j + C::NS, sb);   // S[sb] is free once PV_j (issued above, in order) read P_j
       };
       if constexpr (C::NS == 2) {
@@ -229,19 +209,12 @@ __global__ void __launch_bounds__(320, 1)
     const int q_row0 = qi * block;
     const int q_rows = min(block, N - q_row0);
     float m_run = -INFINITY, l_run = 0.f;
-    int it = 0, tc_ = 0;
+    int it = 0;
     for (int j = g; j < L; j += 2, ++it) {
       const int sb = C::NS == 2 ? g : C::sbuf(j);                 // S_j, then P_j
       const uint32_t t_s = C::NS == 2 ? t_sg : tmem + lane_off + sb * BN;
       mbar_wait(&s_full[sb], C::NS == 2 ? (uint32_t)(it & 1) : C::sphase(j));
-      if (lane == 0 && quarter == 2) trace(dbg, 2 + g, tc_, 20 + g, j);
       tc_fence_after();
-      if (dbg & 1) {   // bring-up: MMA/TMA pipeline without the softmax math
-        if (it >= 1) mbar_wait(&o_done[g], (it - 1) & 1);
-        tc_fence_before();
-        mbar_arrive(&p_full[g]);
-        continue;
-      }
       uint32_t sr[BN];
 #pragma unroll
       for (int c = 0; c < BN / 32; ++c) tmem_ld32(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
@@ -287,7 +260,6 @@ __global__ void __launch_bounds__(320, 1)
       }
       l_run = fmaf(l_run, alpha, (acc2[0].x + acc2[0].y) + (acc2[1].x + acc2[1].y));
       m_run = m_use;
-      if (lane == 0 && quarter == 2) trace(dbg, 2 + g, tc_, 30 + g, j);
 #pragma unroll
       for (int c = 0; c < BN / 64; ++c) tmem_st32(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[c * 32]));
       if (it >= 1) {
@@ -308,7 +280,6 @@ __global__ void __launch_bounds__(320, 1)
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&p_full[g]);
-      if (lane == 0 && quarter == 2) trace(dbg, 2 + g, tc_, 40 + g, j);
     }
     // epilogue: merge the two split-KV partial results, O / l -> bf16, lse
     auto red = reinterpret_cast<float(*)[2][128]>(smem + C::OFF_RED);   // [group][m|l][row]
@@ -368,6 +339,419 @@ __global__ void __launch_bounds__(320, 1)
 }
 
 // ================================================================================================
+// Default K4 schedule (MOD_ATTN_DEFAULT): ONE softmax group of 8 warps, NS S buffers ahead of it.
+//   warp 0      TMA producer (as above): Q once; K_j into ring slot j % NS, V_j into slot j % 2.
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer:  S_0 .. S_{NS-1}, then per j
+//                  [wait P_j, V_j] PV_j -> O      [wait K_{j+NS}] S_{j+NS} -> S[j % NS]
+//               so S_{j+1} .. S_{j+NS-1} and PV_{j-1} are queued while the softmax works on S_j: the
+//               tensor pipe has 2(NS-1) MMA groups (2048 cycles at NS = 3) of work between S_j and PV_j.
+//   warps 2..   softmax, SPLIT warps per SM sub-partition (4 at 128-key blocks, 2 at 64): warp (quarter q,
+//               part h) owns rows [32q, 32q+32) (its TMEM lane quarter) and key columns [32h, 32h+32) of
+//               every block, so each thread exponentiates 32 scores per block, the SPLIT warps of a
+//               sub-partition hide each other's MUFU / FMA latencies, and they share one running max
+//               and one O (whose D columns they split for the rare rescale and the epilogue).
+//               The running max is NOT recomputed per block: the scores are exponentiated against the
+//               current reference max m and the half-row sum tells whether any score exceeded m by
+//               more than 20 (log2 units: p <= sum <= 2^20 -- far from fp32 overflow, exact in the
+//               bf16 P and fp32 l / O that follow).  Only then (first block, or a jump of the row
+//               maximum) do the two warps exchange half-row maxima, redo the block against the new m
+//               and rescale l and O -- the online softmax with a lazily updated reference, which is
+//               exact for any reference (the same result up to rounding).
+//               One named barrier per block among the SPLIT warps of a sub-partition exchanges the
+//               overflow flags and orders all their S loads before any P store (P_j is packed bf16
+//               over the first BN/2 columns of S_j's buffer, the TS operand of PV_j).
+// TMEM: S[b] at [b BN, (b+1) BN) for b < NS, O after them (NS = 3 at D = BN = 128: 512 columns).
+#ifndef K4_WAIT
+#define K4_WAIT mbar_wait_sleep   // producer / MMA-issuer waits (the softmax warps poll)
+#endif
+template <int D, int BN>
+struct Attn1Cfg {
+  static constexpr int BM = 128;
+  static constexpr int NS = (512 - D) / BN > 7 ? 7 : (512 - D) / BN;
+  static constexpr int VSTAGES = 2;
+#ifndef K4_SPLIT
+#define K4_SPLIT 2
+#endif
+  static constexpr int SPLIT = BN == 128 ? K4_SPLIT : 2;   // softmax warps per SM sub-partition (row set)
+  static constexpr int COLS = BN / SPLIT;             // score columns per softmax warp (32)
+  static constexpr int OCOLS = D / SPLIT;             // O columns per softmax warp (rescale, epilogue)
+  static constexpr int Q_BOX = BM * 128, KV_BOX = BN * 128, NATOM = D / 64;
+  static constexpr int Q_BYTES = Q_BOX * NATOM, KV_BYTES = KV_BOX * NATOM;
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = OFF_Q + Q_BYTES;
+  static constexpr int OFF_V = OFF_K + NS * KV_BYTES;
+  static constexpr int OFF_BAR = OFF_V + VSTAGES * KV_BYTES;
+  // q_full, k_full[NS], v_full[2], s_full[NS], p_full[NS], o_done[2]
+  static constexpr int NUM_BARS = 1 + NS + VSTAGES + NS + NS + VSTAGES;
+  static constexpr int OFF_XCH = (OFF_BAR + NUM_BARS * 8 + 16 + 15) / 16 * 16;
+  static constexpr int XCH = 2 * 4 * SPLIT * 32;      // [parity][quarter][part][lane] floats per kind
+  static constexpr int SMEM = OFF_XCH + 3 * XCH * 4;  // kinds: flag, max, l
+  static constexpr int TMEM_O = NS * BN;
+  static constexpr uint32_t TMEM_COLS = (NS * BN + D) <= 256 ? 256 : 512;
+  static constexpr uint32_t IDESC_S = idesc_bf16_f32(BM, BN, false, false);
+  static constexpr uint32_t IDESC_O = idesc_bf16_f32(BM, D, false, true);
+  static constexpr int THREADS = 64 + 128 * SPLIT;    // producer, MMA issuer, 4 x SPLIT softmax warps
+#ifndef K4_EMU
+#define K4_EMU 2
+#endif
+#ifndef K4_EMU1
+#define K4_EMU1 2
+#endif
+  static constexpr int EMU = K4_EMU;                  // pairs of every 8 exponentiated on the FMA pipe
+  static constexpr int EMU1 = K4_EMU1;                // the same on the MMA warp's sub-partition (quarter 1)
+  static constexpr float OVF = 1048576.0f;            // 2^20: half-row sum bound of the lazy reference
+};
+
+// Bring-up instrumentation, compiled only into trace builds (-DMOD_K4_TRACE, scripts/k4_trace.py):
+// clock64 stamps of the MMA thread and of one softmax warp for every 4096th CTA, and per-CTA
+// clock64 / globaltimer spans of every CTA.  The shipped library contains none of it.
+#ifdef MOD_K4_TRACE
+constexpr int kTrCtas = 8, kTrBlocks = 512;
+__device__ long long g_k4_ev[kTrCtas][18][kTrBlocks][6];
+__device__ long long g_k4_span[1 << 16][4];
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define K4T(role, ev, j)                                                                      \
+  do {                                                                                        \
+    if ((blockIdx.x & 4095) == 1234 && (j) < kTrBlocks && (blockIdx.x >> 12) < kTrCtas)       \
+      g_k4_ev[blockIdx.x >> 12][role][j][ev] = clock64();                                     \
+  } while (0)
+#else
+#define K4T(role, ev, j) \
+  do {                   \
+  } while (0)
+#endif
+
+
+template <int EMU, int NC>
+__device__ __forceinline__ float exp_pack(const float* s, float scale_log2, float m, uint32_t* pk) {
+  const float2 sc2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-m, -m);
+  float2 acc2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+  for (int c = 0; c < NC; c += 2) {
+    const float2 x = ffma2(make_float2(s[c], s[c + 1]), sc2, nm2);
+    float2 p;
+    if (((c / 2) & 7) < EMU) {
+      p = ex2_poly2<true>(x);
+    } else {
+      p.x = ex2(x.x);
+      p.y = ex2(x.y);
+    }
+    acc2[(c / 2) & 1] = fadd2(acc2[(c / 2) & 1], p);
+    pk[c / 2] = pack_bf16(p.x, p.y);
+  }
+  return (acc2[0].x + acc2[0].y) + (acc2[1].x + acc2[1].y);
+}
+
+template <int NC>
+__device__ __forceinline__ float row_max(const float* s) {   // max of s[0..NC), two FMNMX3 chains
+  static_assert(NC % 4 == 0, "row_max: NC must be a multiple of 4");
+  float a = s[0], b = s[1];
+#pragma unroll
+  for (int c = 2; c < NC; c += 4) {
+    a = fmax3f(a, s[c], s[c + 1]);
+    if (c + 3 < NC) b = fmax3f(b, s[c + 2], s[c + 3]);
+  }
+  return fmaxf(a, b);
+}
+
+template <int D, int BN>
+__global__ void __launch_bounds__(Attn1Cfg<D, BN>::THREADS, 1)
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                    const __grid_constant__ CUtensorMap tm_v, const int* __restrict__ row_ptr,
+                    const int* __restrict__ col_idx, __nv_bfloat16* __restrict__ out, float* __restrict__ lse,
+                    int N, int n, int block, float scale_log2) {
+  using C = Attn1Cfg<D, BN>;
+  constexpr int NS = C::NS;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = bars + 1;
+  uint64_t* v_full = k_full + NS;
+  uint64_t* s_full = v_full + C::VSTAGES;
+  uint64_t* p_full = s_full + NS;
+  uint64_t* o_done = p_full + NS;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + C::VSTAGES);
+  float* xch = reinterpret_cast<float*>(smem + C::OFF_XCH);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0 && (smem_u32(smem) & 1023u) != 0) __trap();   // SWIZZLE_128B needs 1024B alignment
+  const int item = blockIdx.x;
+  const int bh = item / n, qi = item % n;
+  const int beg = row_ptr[(size_t)bh * (n + 1) + qi];
+  const int L = row_ptr[(size_t)bh * (n + 1) + qi + 1] - beg;
+  const int* cols = col_idx + (size_t)bh * n * n + beg;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&s_full[s], 1);
+      mbar_init(&p_full[s], 4 * C::SPLIT);   // one elected arrival per softmax warp
+    }
+    for (int s = 0; s < C::VSTAGES; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&o_done[s], 1);
+    }
+    fence_mbar_init();
+  }
+#ifdef MOD_K4_TRACE
+  const long long span_c0 = clock64(), span_t0 = gtimer();
+#endif
+  if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0 && L > 0) {
+      tma_prefetch_desc(&tm_q);
+      tma_prefetch_desc(&tm_k);
+      tma_prefetch_desc(&tm_v);
+      const uint64_t pol_q = policy_evict_first(), pol_kv = policy_evict_last();
+      mbar_arrive_expect_tx(q_full, C::Q_BYTES);
+#pragma unroll
+      for (int a = 0; a < C::NATOM; ++a)
+        tma_load_3d(smem + C::OFF_Q + a * C::Q_BOX, &tm_q, q_full, a * 64, qi * block, bh, pol_q);
+      auto load_k = [&](int j) {
+        const int s = j % NS;
+        if (j >= NS) K4_WAIT(&s_full[s], ((j / NS) - 1) & 1);   // S_{j-NS} has consumed K slot s
+#ifdef K4_NO_KV
+        mbar_arrive(&k_full[s]);
+        return;
+#endif
+        unsigned char* dst = smem + C::OFF_K + s * C::KV_BYTES;
+        mbar_arrive_expect_tx(&k_full[s], C::KV_BYTES);
+        const int row = cols[j] * block;
+#pragma unroll
+        for (int a = 0; a < C::NATOM; ++a) tma_load_3d(dst + a * C::KV_BOX, &tm_k, &k_full[s], a * 64, row, bh, pol_kv);
+      };
+      auto load_v = [&](int j) {
+        const int s = j & 1;
+        if (j >= 2) K4_WAIT(&o_done[s], ((j >> 1) - 1) & 1);    // PV_{j-2} has consumed V slot s
+#ifdef K4_NO_KV
+        mbar_arrive(&v_full[s]);
+        return;
+#endif
+        unsigned char* dst = smem + C::OFF_V + s * C::KV_BYTES;
+        mbar_arrive_expect_tx(&v_full[s], C::KV_BYTES);
+        const int row = cols[j] * block;
+#pragma unroll
+        for (int a = 0; a < C::NATOM; ++a) tma_load_3d(dst + a * C::KV_BOX, &tm_v, &v_full[s], a * 64, row, bh, pol_kv);
+      };
+      // demand order of the MMA warp: K_0 .. K_{NS-1}, then V_j, K_{j+NS} for j = 0, 1, ...
+      for (int j = 0; j < NS && j < L; ++j) load_k(j);
+      for (int j = 0; j < L; ++j) {
+        load_v(j);
+        if (j + NS < L) load_k(j + NS);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    // The whole warp runs this loop converged and elect.sync picks the issuing lane inside each MMA, so
+    // descriptors stay in uniform registers and an MMA costs ~2 instructions: this warp shares its SM
+    // sub-partition's issue slots with SPLIT softmax warps, and every extra instruction per MMA delays
+    // the tensor pipe (scripts/micro/mma_probe.cu: 1037 -> 1650 cycles per block with 4 busy neighbours).
+    if (L > 0) {
+      const uint32_t sq = smem_u32(smem + C::OFF_Q);
+      K4_WAIT(q_full, 0);
+      tc_fence_after();
+      const uint64_t a_base = smem_desc_sw128(sq, 16, 1024);
+      auto issue_s = [&](int j, auto bc) {   // bc: compile-time S buffer index j % NS
+        constexpr int b = decltype(bc)::value;
+        K4_WAIT(&k_full[b], (j / NS) & 1);
+        tc_fence_after();
+        const uint64_t b_base = smem_desc_sw128(smem_u32(smem + C::OFF_K + b * C::KV_BYTES), 16, 1024);
+        // K-major SW128: 32 bytes per K step inside a 128B atom, atoms one box apart (offsets in 16 B)
+        static_for<D / 16>([&](auto kc) {
+          constexpr int kk = decltype(kc)::value;
+          mma_ss_e<((kk / 4) * C::Q_BOX + (kk % 4) * 32) / 16, ((kk / 4) * C::KV_BOX + (kk % 4) * 32) / 16>(
+              tmem + b * BN, a_base, b_base, C::IDESC_S, kk > 0 ? 1u : 0u);
+        });
+        mma_commit_e(&s_full[b]);          // also releases K slot b to the producer
+      };
+      auto pv_then_s = [&](int j, auto bc, auto vc) {   // b = j % NS, vs = j % 2 (compile time)
+        constexpr int b = decltype(bc)::value, vs = decltype(vc)::value;
+        K4T(0, 0, j);
+        K4_WAIT(&v_full[vs], (j >> 1) & 1);
+        K4T(0, 1, j);
+        K4_WAIT(&p_full[b], (j / NS) & 1);
+        K4T(0, 2, j);
+        tc_fence_after();
+        const uint64_t v_base = smem_desc_sw128(smem_u32(smem + C::OFF_V + vs * C::KV_BYTES), C::KV_BOX, 1024);
+        const uint32_t acc0 = j > 0 ? 1u : 0u;
+        // B = V_j: N = D (MN-major, 64-column atoms LBO = KV_BOX apart), K = 16 keys = 2048 bytes
+        static_for<BN / 16>([&](auto kc) {
+          constexpr int kk = decltype(kc)::value;
+          mma_ts_e<kk * 8, kk * 2048 / 16>(tmem + C::TMEM_O, tmem + b * BN, v_base, C::IDESC_O, kk > 0 ? 1u : acc0);
+        });
+        mma_commit_e(&o_done[vs]);         // also releases V slot vs to the producer
+        K4T(0, 3, j);
+        if (j + NS < L) issue_s(j + NS, bc);   // S buffer b is free once PV_j (issued above, in order) read P_j
+        K4T(0, 4, j);
+      };
+      static_for<NS>([&](auto bc) {
+        constexpr int b0 = decltype(bc)::value;
+        if (b0 < L) issue_s(b0, bc);
+      });
+      // unrolled over lcm(NS, 2) blocks so that the S buffer and V slot of every step are literals
+      constexpr int U = (NS % 2) ? 2 * NS : NS;
+      for (int j0 = 0; j0 < L; j0 += U) {
+        static_for<U>([&](auto uc) {
+          constexpr int u = decltype(uc)::value;
+          if (j0 + u < L) pv_then_s(j0 + u, std::integral_constant<int, u % NS>{}, std::integral_constant<int, u % 2>{});
+        });
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ softmax / epilogue (4 x SPLIT warps)
+    constexpr int SPLIT = C::SPLIT, COLS = C::COLS, OCOLS = C::OCOLS, OCH = OCOLS < 32 ? OCOLS : 32;
+    const int quarter = warp & 3;           // TMEM lane quarter this warp may access
+    const int h = (warp - 2) >> 2;          // key-column part of every block (and D part of O)
+    const int row = quarter * 32 + lane;    // query row within the tile
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const uint32_t bar_id = 1 + quarter;    // named barrier of the SPLIT warps sharing these rows
+    auto X = [&](int kind, int par, int hh) -> float& {
+      return xch[kind * C::XCH + ((par * 4 + quarter) * SPLIT + hh) * 32 + lane];
+    };
+    auto xmax = [&](int kind, int par) {
+      float m = X(kind, par, 0);
+#pragma unroll
+      for (int hh = 1; hh < SPLIT; ++hh) m = fmaxf(m, X(kind, par, hh));
+      return m;
+    };
+    const int q_row0 = qi * block;
+    const int q_rows = min(block, N - q_row0);
+    float m_run = -INFINITY, l_run = 0.f;   // reference max (log2 units, scaled) / this part's row sum
+    const bool tr = lane == 0;
+    const int trole = warp - 1;   // trace role of this softmax warp (1..)
+#pragma unroll 1
+    for (int j = 0; j < L; ++j) {
+      const int b = j % NS;
+      if (tr) K4T(trole, 0, j);
+      mbar_wait(&s_full[b], (j / NS) & 1);
+      if (tr) K4T(trole, 1, j);
+      tc_fence_after();
+      uint32_t sr[COLS];
+      tmem_ldn<COLS>(tmem + lane_off + b * BN + h * COLS, sr);
+      tmem_ld_wait();
+      float* s = reinterpret_cast<float*>(sr);
+      const int kv_valid = N - cols[j] * block - h * COLS;   // keys of this part inside the sequence
+      if (kv_valid < COLS) {
+#pragma unroll
+        for (int c = 0; c < COLS; ++c)
+          if (c >= kv_valid) s[c] = -INFINITY;
+      }
+      if (j == 0) {   // first block of the list: the exact row maximum (all parts)
+        X(1, 0, h) = row_max<COLS>(s) * scale_log2;
+        named_bar_sync(bar_id, 32 * SPLIT);
+        m_run = xmax(1, 0);                  // finite: every listed block holds >= 1 key
+      }
+      if (tr) K4T(trole, 2, j);
+      uint32_t pk[COLS / 2];
+      float sum = quarter == 1 ? exp_pack<C::EMU1, COLS>(s, scale_log2, m_run, pk)
+                               : exp_pack<C::EMU, COLS>(s, scale_log2, m_run, pk);
+      const bool need = !(sum <= C::OVF);
+      if (tr) K4T(trole, 3, j);
+      // any overflow among the SPLIT parts of these 32 rows?  Also orders every part's S_j load
+      // before any P_j store (P_j is packed over the first BN/2 columns of S_j's buffer).
+      const bool any_need = named_bar_or(bar_id, 32 * SPLIT, need);
+      if (tr) K4T(trole, 4, j);
+      if (any_need) {
+        // rare: a row maximum moved up by > 20 (log2): exchange part maxima per row, redo against the new m
+        const int par = j & 1;
+        X(0, par, h) = need ? 1.f : 0.f;
+        X(1, par, h) = row_max<COLS>(s) * scale_log2;
+        named_bar_sync(bar_id, 32 * SPLIT);
+        const bool need_row = xmax(0, par) != 0.f;
+        const float m_new = need_row ? fmaxf(m_run, xmax(1, par)) : m_run;
+        const float alpha = ex2(m_run - m_new);
+        if (need_row) sum = exp_pack<0, COLS>(s, scale_log2, m_new, pk);
+        l_run *= alpha;
+        m_run = m_new;
+        if (j > 0 && __any_sync(0xffffffffu, alpha < 1.f)) {
+          mbar_wait(&o_done[(j - 1) & 1], ((j - 1) >> 1) & 1);   // PV_{j-1} has written O
+          tc_fence_after();
+          const uint32_t t_o = tmem + lane_off + C::TMEM_O + h * OCOLS;
+#pragma unroll
+          for (int c = 0; c < OCOLS / OCH; ++c) {
+            uint32_t o[OCH];
+            tmem_ldn<OCH>(t_o + c * OCH, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < OCH; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+            tmem_stn<OCH>(t_o + c * OCH, o);
+          }
+        }
+        named_bar_sync(bar_id, 32 * SPLIT);   // the exchange slots of this parity are read by all
+      }
+      l_run += sum;
+      tmem_stn<COLS / 2>(tmem + lane_off + b * BN + h * (COLS / 2), pk);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[b]);
+      if (tr) K4T(trole, 5, j);
+    }
+    // epilogue: l = sum of the parts' sums (they share m), O / l -> bf16 (this warp's D part), lse
+    X(2, 0, h) = l_run;
+    named_bar_sync(bar_id, 32 * SPLIT);
+    float l = 0.f;
+#pragma unroll
+    for (int hh = 0; hh < SPLIT; ++hh) l += X(2, 0, hh);
+    const bool valid = row < q_rows;
+    const size_t grow = (size_t)bh * N + q_row0 + row;
+    if (L > 0) {
+      mbar_wait(&o_done[(L - 1) & 1], ((L - 1) >> 1) & 1);
+      tc_fence_after();
+      const float inv = 1.0f / l;
+      const uint32_t t_o = tmem + lane_off + C::TMEM_O + h * OCOLS;
+#pragma unroll
+      for (int c = 0; c < OCOLS / OCH; ++c) {
+        uint32_t o[OCH];
+        tmem_ldn<OCH>(t_o + c * OCH, o);
+        tmem_ld_wait();
+        uint32_t pkd[OCH / 2];
+#pragma unroll
+        for (int e = 0; e < OCH / 2; ++e) pkd[e] = pack_bf16(__uint_as_float(o[2 * e]) * inv, __uint_as_float(o[2 * e + 1]) * inv);
+        if (valid) {
+          int4* dst = reinterpret_cast<int4*>(out + grow * D + h * OCOLS + c * OCH);
+#pragma unroll
+          for (int e = 0; e < OCH / 8; ++e) dst[e] = make_int4(pkd[4 * e], pkd[4 * e + 1], pkd[4 * e + 2], pkd[4 * e + 3]);
+        }
+      }
+      if (valid && lse && h == 0) lse[grow] = (m_run + __log2f(l)) * 0.69314718055994531f;
+    } else if (valid) {
+      int4* dst = reinterpret_cast<int4*>(out + grow * D + h * OCOLS);
+#pragma unroll
+      for (int e = 0; e < OCOLS / 8; ++e) dst[e] = make_int4(0, 0, 0, 0);
+      if (lse && h == 0) lse[grow] = -INFINITY;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<C::TMEM_COLS>(tmem);
+  }
+#ifdef MOD_K4_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < (1 << 16)) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_k4_span[blockIdx.x][0] = clock64() - span_c0;
+    g_k4_span[blockIdx.x][1] = gtimer() - span_t0;
+    g_k4_span[blockIdx.x][2] = span_t0;
+    g_k4_span[blockIdx.x][3] = ((long long)smid << 32) | (unsigned)L;
+  }
+#endif
+}
+
+// ================================================================================================
 // Paired query blocks: one CTA per (b, h, pair of query blocks 2p, 2p+1).
 // Adjacent rows of the MOD-DiT mask share most of their index lists (vertical columns, frame
 // squares, diagonals whose neighbour offset is also selected: 79 % at Hunyuan 720p, Family S), so the
@@ -410,7 +794,7 @@ __global__ void __launch_bounds__(320, 1)
     attn_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                      const __grid_constant__ CUtensorMap tm_v, const int* __restrict__ row_ptr,
                      const int* __restrict__ col_idx, __nv_bfloat16* __restrict__ out, float* __restrict__ lse,
-                     int N, int n, float scale_log2, int dbg) {
+                     int N, int n, float scale_log2) {
   using C = PairCfg<D, BN>;
   extern __shared__ __align__(1024) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
@@ -500,7 +884,6 @@ __global__ void __launch_bounds__(320, 1)
       const uint32_t sq = smem_u32(smem + C::OFF_Q);
       mbar_wait(q_full, 0);
       // scalar state (no dynamically indexed arrays: they would live in local memory)
-      int tc_ = 0;
       int pend0 = -1, pend1 = -1;      // stream entry of tile X's issued S whose PV is still due
       int npv0 = 0, npv1 = 0;          // PVs issued per tile (phase of p_full[X])
       int vrem0 = 0, vrem1 = 0;        // PVs still to read V slot 0 / 1
@@ -509,7 +892,6 @@ __global__ void __launch_bounds__(320, 1)
         const int np = X ? npv1 : npv0;
         mbar_wait(&v_full[s], (e >> 1) & 1);
         mbar_wait(&p_full[X], np & 1);
-        trace(dbg, 1, tc_, 12 + 2 * X, e);
         tc_fence_after();
         const uint32_t sv = smem_u32(smem + C::OFF_V + s * C::KV_BYTES);
         const uint32_t p_t = tmem + C::TMEM_S + X * BN;
@@ -561,7 +943,6 @@ __global__ void __launch_bounds__(320, 1)
         if (u & 1) vrem1 = (int)fa + (int)fb; else vrem0 = (int)fa + (int)fb;
         kwait = false;
         // FA4-style interleave when both lists hold u: PV_A, S_A(u), PV_B, S_B(u)
-        trace(dbg, 1, tc_, 10, u);
         if (fa) {
           if (pend0 >= 0) emit_pv(0);
           emit_s(0, u);
@@ -570,7 +951,6 @@ __global__ void __launch_bounds__(320, 1)
           if (pend1 >= 0) emit_pv(1);
           emit_s(1, u);
         }
-        trace(dbg, 1, tc_, 13, u);
         mma_commit(&k_empty[u & 1]);   // both S of entry u issued: K slot free once they complete
         ++u;
       }
@@ -588,10 +968,8 @@ __global__ void __launch_bounds__(320, 1)
     const int LX = X ? LB : LA;
     const uint16_t* lx = X ? lb : la;
     float m_run = -INFINITY, l_run = 0.f;
-    int tc_ = 0;
     for (int j = 0; j < LX; ++j) {
       mbar_wait(&s_full[X], j & 1);
-      if (lane == 0 && quarter == 2) trace(dbg, 2 + X, tc_, 20 + X, j);
       tc_fence_after();
       uint32_t sr[BN];
 #pragma unroll
@@ -652,7 +1030,6 @@ __global__ void __launch_bounds__(320, 1)
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&p_full[X]);
-      if (lane == 0 && quarter == 2) trace(dbg, 2 + X, tc_, 40 + X, j);
     }
     // epilogue: O_X / l -> bf16, lse (no merge: each tile owns its accumulator)
     if (qx < n) {
@@ -697,223 +1074,6 @@ __global__ void __launch_bounds__(320, 1)
 
 
 // ================================================================================================
-// Two CTAs per SM, one softmax chain each (MOD_ATTN_KERNEL=dual).  The single kernel above holds one
-// query block per SM with two split-KV softmax groups, so each CTA's pipeline fill (Q load, first S,
-// first softmax) and epilogue (last PV, merge, O store) leave the tensor pipe idle; here a CTA owns
-// ONE chain  S_j -> softmax_j -> PV_j -> S_{j+1}  (TMEM: S [0,BN), O [BN,BN+D) = 256 columns; one-slot
-// K and V buffers, refilled while the chain's softmax runs: 96 KB of shared memory), and two CTAs
-// share each SM, so the two chains interleave on the tensor pipe and one CTA's fill / epilogue
-// overlaps the other's steady state.
-template <int D, int BN>
-struct DualCfg {
-  static constexpr int BM = 128;
-  static constexpr int Q_BOX = BM * 128, KV_BOX = BN * 128, NATOM = D / 64;
-  static constexpr int Q_BYTES = Q_BOX * NATOM, KV_BYTES = KV_BOX * NATOM;
-  static constexpr int OFF_Q = 0, OFF_K = Q_BYTES, OFF_V = OFF_K + KV_BYTES, OFF_BAR = OFF_V + KV_BYTES;
-  static constexpr int NUM_BARS = 6;   // q_full, k_full, v_full, s_full, p_full, o_done
-  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;
-  static constexpr int TMEM_S = 0, TMEM_O = BN;
-  static constexpr uint32_t TMEM_COLS = (BN + D) <= 128 ? 128 : 256;
-  static constexpr uint32_t IDESC_S = idesc_bf16_f32(BM, BN, false, false);
-  static constexpr uint32_t IDESC_O = idesc_bf16_f32(BM, D, false, true);
-  static constexpr int THREADS = 192;
-};
-
-template <int D, int BN>
-__global__ void __launch_bounds__(192, 2)
-    attn_dual_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                     const __grid_constant__ CUtensorMap tm_v, const int* __restrict__ row_ptr,
-                     const int* __restrict__ col_idx, __nv_bfloat16* __restrict__ out, float* __restrict__ lse,
-                     int N, int n, int block, float scale_log2) {
-  using C = DualCfg<D, BN>;
-  extern __shared__ __align__(1024) unsigned char smem[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
-  uint64_t* q_full = bars;
-  uint64_t* k_full = bars + 1;
-  uint64_t* v_full = bars + 2;
-  uint64_t* s_full = bars + 3;
-  uint64_t* p_full = bars + 4;
-  uint64_t* o_done = bars + 5;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6);
-
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int item = blockIdx.x;
-  const int bh = item / n, qi = item % n;
-  const int beg = row_ptr[(size_t)bh * (n + 1) + qi];
-  const int L = row_ptr[(size_t)bh * (n + 1) + qi + 1] - beg;
-  const int* cols = col_idx + (size_t)bh * n * n + beg;
-
-  if (threadIdx.x == 0) {
-    mbar_init(q_full, 1);
-    mbar_init(k_full, 1);
-    mbar_init(v_full, 1);
-    mbar_init(s_full, 1);
-    mbar_init(p_full, 128);
-    mbar_init(o_done, 1);
-    fence_mbar_init();
-  }
-  if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
-    if (lane == 0 && L > 0) {
-      const uint64_t pol_q = policy_evict_first(), pol_kv = policy_evict_last();
-      mbar_arrive_expect_tx(q_full, C::Q_BYTES);
-#pragma unroll
-      for (int a = 0; a < C::NATOM; ++a)
-        tma_load_3d(smem + C::OFF_Q + a * C::Q_BOX, &tm_q, q_full, a * 64, qi * block, bh, pol_q);
-      for (int j = 0; j < L; ++j) {
-        const int row = cols[j] * block;
-        if (j >= 1) mbar_wait(s_full, (j - 1) & 1);   // S_{j-1} has read K_{j-1}
-        mbar_arrive_expect_tx(k_full, C::KV_BYTES);
-#pragma unroll
-        for (int a = 0; a < C::NATOM; ++a) tma_load_3d(smem + C::OFF_K + a * C::KV_BOX, &tm_k, k_full, a * 64, row, bh, pol_kv);
-        if (j >= 1) mbar_wait(o_done, (j - 1) & 1);   // PV_{j-1} has read V_{j-1}
-        mbar_arrive_expect_tx(v_full, C::KV_BYTES);
-#pragma unroll
-        for (int a = 0; a < C::NATOM; ++a) tma_load_3d(smem + C::OFF_V + a * C::KV_BOX, &tm_v, v_full, a * 64, row, bh, pol_kv);
-      }
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer: S_j, [P_j] PV_j, S_{j+1}, ...
-    if (lane == 0 && L > 0) {
-      const uint32_t sq = smem_u32(smem + C::OFF_Q), sk = smem_u32(smem + C::OFF_K), sv = smem_u32(smem + C::OFF_V);
-      mbar_wait(q_full, 0);
-      for (int j = 0; j < L; ++j) {
-        mbar_wait(k_full, j & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint64_t ad = smem_desc_sw128(sq + (kk / 4) * C::Q_BOX + (kk % 4) * 32, 16, 1024);
-          const uint64_t bd = smem_desc_sw128(sk + (kk / 4) * C::KV_BOX + (kk % 4) * 32, 16, 1024);
-          mma_ss(tmem + C::TMEM_S, ad, bd, C::IDESC_S, kk > 0 ? 1u : 0u);
-        }
-        mma_commit(s_full);
-        mbar_wait(v_full, j & 1);
-        mbar_wait(p_full, j & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < BN / 16; ++kk) {
-          const uint64_t bd = smem_desc_sw128(sv + kk * 2048, C::KV_BOX, 1024);
-          mma_ts(tmem + C::TMEM_O, tmem + C::TMEM_S + kk * 8, bd, C::IDESC_O, (j > 0 || kk > 0) ? 1u : 0u);
-        }
-        mma_commit(o_done);
-      }
-    }
-  } else {
-    // ------------------------------------------------------------ softmax / epilogue (warps 2..5)
-    const int quarter = warp & 3;
-    const int row = quarter * 32 + lane;
-    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-    const uint32_t t_s = tmem + lane_off + C::TMEM_S;
-    const uint32_t t_o = tmem + lane_off + C::TMEM_O;
-    const int q_row0 = qi * block;
-    float m_run = -INFINITY, l_run = 0.f;
-    for (int j = 0; j < L; ++j) {
-      mbar_wait(s_full, j & 1);
-      tc_fence_after();
-      uint32_t sr[BN];
-#pragma unroll
-      for (int c = 0; c < BN / 32; ++c) tmem_ld32(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
-      tmem_ld_wait();
-      float* s = reinterpret_cast<float*>(sr);
-      const int kv_valid = N - cols[j] * block;
-      if (kv_valid < BN) {
-#pragma unroll
-        for (int c = 0; c < BN; ++c)
-          if (c >= kv_valid) s[c] = -INFINITY;
-      }
-      float mxv[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) mxv[u] = s[u];
-#pragma unroll
-      for (int c = 8; c < BN; c += 8)
-#pragma unroll
-        for (int u = 0; u < 8; ++u) mxv[u] = fmaxf(mxv[u], s[c + u]);
-      const float mx = fmaxf(fmaxf(fmaxf(mxv[0], mxv[1]), fmaxf(mxv[2], mxv[3])),
-                             fmaxf(fmaxf(mxv[4], mxv[5]), fmaxf(mxv[6], mxv[7])));
-      const float m_new = fmaxf(m_run, mx * scale_log2);
-      const bool rescale = (m_new - m_run) > 8.0f;
-      const float m_use = rescale ? m_new : m_run;
-      const float alpha = rescale ? ex2(m_run - m_new) : 1.0f;
-      const float2 sc2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-m_use, -m_use);
-      float2 acc2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-      uint32_t pk[BN / 2];
-#pragma unroll
-      for (int c = 0; c < BN; c += 2) {
-        const float2 x = ffma2(make_float2(s[c], s[c + 1]), sc2, nm2);
-        float2 p;
-        if (((c / 2) & 7) < kEmuPairsPer8) {
-          p = ex2_poly2(x);
-        } else {
-          p.x = ex2(x.x);
-          p.y = ex2(x.y);
-        }
-        acc2[(c / 2) & 1] = fadd2(acc2[(c / 2) & 1], p);
-        pk[c / 2] = pack_bf16(p.x, p.y);
-      }
-      l_run = fmaf(l_run, alpha, (acc2[0].x + acc2[0].y) + (acc2[1].x + acc2[1].y));
-      m_run = m_use;
-#pragma unroll
-      for (int c = 0; c < BN / 64; ++c) tmem_st32(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[c * 32]));
-      // S_j was issued after PV_{j-1}: s_full above already implies O holds PV_{j-1}
-      if (j >= 1 && __any_sync(0xffffffffu, rescale)) {
-#pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t o[32];
-          tmem_ld32(t_o + c * 32, o);
-          tmem_ld_wait();
-#pragma unroll
-          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-          tmem_st32(t_o + c * 32, o);
-        }
-      }
-      tmem_st_wait();
-      tc_fence_before();
-      mbar_arrive(p_full);
-    }
-    const bool valid = row < min(block, N - q_row0);
-    const size_t grow = (size_t)bh * N + q_row0 + row;
-    if (L > 0) {
-      mbar_wait(o_done, (L - 1) & 1);
-      tc_fence_after();
-      const float inv = 1.0f / l_run;
-#pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t o[32];
-        tmem_ld32(t_o + c * 32, o);
-        tmem_ld_wait();
-        uint32_t pkd[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e)
-          pkd[e] = pack_bf16(__uint_as_float(o[2 * e]) * inv, __uint_as_float(o[2 * e + 1]) * inv);
-        if (valid) {
-          int4* dst = reinterpret_cast<int4*>(out + grow * D + c * 32);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) dst[e] = make_int4(pkd[4 * e], pkd[4 * e + 1], pkd[4 * e + 2], pkd[4 * e + 3]);
-        }
-      }
-      if (valid && lse) lse[grow] = (m_run + __log2f(l_run)) * 0.69314718055994531f;
-    } else if (valid) {
-      int4* dst = reinterpret_cast<int4*>(out + grow * D);
-#pragma unroll
-      for (int e = 0; e < D / 8; ++e) dst[e] = make_int4(0, 0, 0, 0);
-      if (lse) lse[grow] = -INFINITY;
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc<C::TMEM_COLS>(tmem);
-  }
-}
-
-
 // ================================================================================================
 // CTA-pair K4 (MOD_ATTN_KERNEL=pair2; D = 128, 128-token blocks): a cluster of 2 CTAs on the two SMs
 // of a TPC owns query blocks 2p (CTA 0, the leader) and 2p+1 (CTA 1).  The leader's single thread
@@ -1274,24 +1434,34 @@ mod_status make_map(CUtensorMap* m, const void* base, int BH, int N, int D, int 
   return MOD_OK;
 }
 
-template <int D, int BN>
-mod_status launch(mod_plan P, const void* q, const void* k, const void* v, const int* row_ptr, const int* col_idx,
-                  void* o, float* lse, cudaStream_t s) {
-  using C = AttnCfg<D, BN>;
+// One launcher for the single-query-block schedules (DEFAULT, SPLITKV): grid = (b, h, query block).
+template <typename Cfg, typename Kern>
+mod_status launch_rows(mod_plan P, Kern kern, int D, int BN, const void* q, const void* k, const void* v,
+                       const int* row_ptr, const int* col_idx, void* o, float* lse, cudaStream_t s) {
   const int BH = P->L.batch * P->L.heads;
   CUtensorMap tq, tk, tv;
   mod_status st;
-  if ((st = make_map(&tq, q, BH, P->N, D, C::BM)) != MOD_OK) return st;
+  if ((st = make_map(&tq, q, BH, P->N, D, Cfg::BM)) != MOD_OK) return st;
   if ((st = make_map(&tk, k, BH, P->N, D, BN)) != MOD_OK) return st;
   if ((st = make_map(&tv, v, BH, P->N, D, BN)) != MOD_OK) return st;
-  auto kern = attn_fwd_kernel<D, BN>;
-  MOD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+  MOD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
   const float scale_log2 = P->scale * 1.4426950408889634f;
-  static const int dbg = getenv("MOD_ATTN_DEBUG") ? atoi(getenv("MOD_ATTN_DEBUG")) : 0;   // bring-up only
-  kern<<<BH * P->n, C::THREADS, C::SMEM, s>>>(tq, tk, tv, row_ptr, col_idx, (__nv_bfloat16*)o, lse, P->N, P->n,
-                                              P->L.block, scale_log2, dbg);
+  kern<<<BH * P->n, Cfg::THREADS, Cfg::SMEM, s>>>(tq, tk, tv, row_ptr, col_idx, (__nv_bfloat16*)o, lse, P->N, P->n,
+                                                  P->L.block, scale_log2);
   MOD_LAUNCH_CHECK();
   return MOD_OK;
+}
+
+template <int D, int BN>
+mod_status launch_default(mod_plan P, const void* q, const void* k, const void* v, const int* row_ptr,
+                          const int* col_idx, void* o, float* lse, cudaStream_t s) {
+  return launch_rows<Attn1Cfg<D, BN>>(P, attn_fwd_kernel<D, BN>, D, BN, q, k, v, row_ptr, col_idx, o, lse, s);
+}
+
+template <int D, int BN>
+mod_status launch_split(mod_plan P, const void* q, const void* k, const void* v, const int* row_ptr,
+                        const int* col_idx, void* o, float* lse, cudaStream_t s) {
+  return launch_rows<SplitCfg<D, BN>>(P, attn_split_kernel<D, BN>, D, BN, q, k, v, row_ptr, col_idx, o, lse, s);
 }
 
 template <int D>
@@ -1310,45 +1480,10 @@ mod_status launch_pair(mod_plan P, const void* q, const void* k, const void* v, 
   MOD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const float scale_log2 = P->scale * 1.4426950408889634f;
   const int npair = (P->n + 1) / 2;
-  static const int dbg = getenv("MOD_ATTN_DEBUG") ? atoi(getenv("MOD_ATTN_DEBUG")) : 0;   // bring-up only
   kern<<<BH * npair, C::THREADS, smem, s>>>(tq, tk, tv, row_ptr, col_idx, (__nv_bfloat16*)o, lse, P->N, P->n,
-                                            scale_log2, dbg);
+                                            scale_log2);
   MOD_LAUNCH_CHECK();
   return MOD_OK;
-}
-
-// K4 variant: one query block per CTA (default) or paired query blocks (MOD_ATTN_KERNEL=pair; only
-// for 128-token blocks and n within the pair kernel's shared-memory list capacity).  Measured at
-// Hunyuan 720p the two run at the same speed (profiles/r1/README.md, "Paired query blocks").
-bool use_pair_kernel(mod_plan P) {
-  const char* e = getenv("MOD_ATTN_KERNEL");   // read per call: tests switch kernels in-process
-  if (!(e && strcmp(e, "pair") == 0) || P->L.block != 128) return false;
-  const int cap = P->L.head_dim == 128 ? PairCfg<128, 128>::MAX_LIST : PairCfg<64, 128>::MAX_LIST;
-  return P->n <= cap && P->n <= 65535;
-}
-
-template <int D, int BN>
-mod_status launch_dual(mod_plan P, const void* q, const void* k, const void* v, const int* row_ptr, const int* col_idx,
-                       void* o, float* lse, cudaStream_t s) {
-  using C = DualCfg<D, BN>;
-  const int BH = P->L.batch * P->L.heads;
-  CUtensorMap tq, tk, tv;
-  mod_status st;
-  if ((st = make_map(&tq, q, BH, P->N, D, C::BM)) != MOD_OK) return st;
-  if ((st = make_map(&tk, k, BH, P->N, D, BN)) != MOD_OK) return st;
-  if ((st = make_map(&tv, v, BH, P->N, D, BN)) != MOD_OK) return st;
-  auto kern = attn_dual_kernel<D, BN>;
-  MOD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-  const float scale_log2 = P->scale * 1.4426950408889634f;
-  kern<<<BH * P->n, C::THREADS, C::SMEM, s>>>(tq, tk, tv, row_ptr, col_idx, (__nv_bfloat16*)o, lse, P->N, P->n,
-                                              P->L.block, scale_log2);
-  MOD_LAUNCH_CHECK();
-  return MOD_OK;
-}
-
-bool use_dual_kernel() {
-  const char* e = getenv("MOD_ATTN_KERNEL");
-  return e && strcmp(e, "dual") == 0;
 }
 
 mod_status launch_pair2(mod_plan P, const void* q, const void* k, const void* v, const int* row_ptr,
@@ -1374,21 +1509,43 @@ mod_status launch_pair2(mod_plan P, const void* q, const void* k, const void* v,
   return MOD_OK;
 }
 
-bool use_pair2_kernel(mod_plan P) {
-  const char* e = getenv("MOD_ATTN_KERNEL");
-  return e && strcmp(e, "pair2") == 0 && P->L.head_dim == 128 && P->L.block == 128;
+// The schedule a plan runs: its config's attn_kernel where that variant supports the layout (pair:
+// 128-token blocks, both lists in shared memory; pair2: additionally D = 128), else the default.
+int effective_kernel(mod_plan P) {
+  const int want = P->cfg.attn_kernel;
+  if (want == MOD_ATTN_PAIR) {
+    const int cap = P->L.head_dim == 128 ? PairCfg<128, 128>::MAX_LIST : PairCfg<64, 128>::MAX_LIST;
+    if (P->L.block == 128 && P->n <= cap && P->n <= 65535) return MOD_ATTN_PAIR;
+    return MOD_ATTN_DEFAULT;
+  }
+  if (want == MOD_ATTN_PAIR2) return (P->L.head_dim == 128 && P->L.block == 128) ? MOD_ATTN_PAIR2 : MOD_ATTN_DEFAULT;
+  return want;
 }
 }  // namespace
 
-// bring-up only (not in moddit.h): copies the trace of the last MOD_ATTN_DEBUG&16 launch
-extern "C" int mod_debug_attn_trace(long long* host, int cap) {
-  // host receives [4][kTraceCap][2]; unused slots are zero
-  if (cap < 5 * kTraceCap * 2) return -1;
-  cudaMemcpyFromSymbol(host, g_trace, sizeof(long long) * 5 * kTraceCap * 2);
-  cudaMemset(nullptr, 0, 0);
-  static long long zeros[5 * kTraceCap * 2];
-  cudaMemcpyToSymbol(g_trace, zeros, sizeof(zeros));
-  return 5 * kTraceCap;
+#ifdef MOD_K4_TRACE
+// trace builds only: copy out the event stamps [kTrCtas][18][kTrBlocks][6] and the CTA spans [n][4]
+extern "C" int mod_debug_k4_trace(long long* ev, long long* span, int n_span) {
+  cudaMemcpyFromSymbol(ev, g_k4_ev, sizeof(g_k4_ev));
+  cudaMemcpyFromSymbol(span, g_k4_span, sizeof(long long) * 4 * (size_t)n_span);
+  return kTrBlocks;
+}
+#endif
+
+
+extern "C" const char* mod_attn_kernel_name(mod_plan P) {
+  if (mod_validate_plan(P) != MOD_OK) return "";
+  const int D = P->L.head_dim, BN = P->L.block;
+  switch (effective_kernel(P)) {
+    case MOD_ATTN_SPLITKV:
+      return D == 128 ? (BN == 128 ? "attn_split_kernel<128,128>" : "attn_split_kernel<128,64>")
+                      : (BN == 128 ? "attn_split_kernel<64,128>" : "attn_split_kernel<64,64>");
+    case MOD_ATTN_PAIR: return D == 128 ? "attn_pair_kernel<128,128>" : "attn_pair_kernel<64,128>";
+    case MOD_ATTN_PAIR2: return "attn_pair2_kernel<128>";
+    default:
+      return D == 128 ? (BN == 128 ? "attn_fwd_kernel<128,128>" : "attn_fwd_kernel<128,64>")
+                      : (BN == 128 ? "attn_fwd_kernel<64,128>" : "attn_fwd_kernel<64,64>");
+  }
 }
 
 extern "C" mod_status mod_block_sparse_attn_fwd(mod_plan P, const void* q, const void* k, const void* v,
@@ -1402,19 +1559,26 @@ extern "C" mod_status mod_block_sparse_attn_fwd(mod_plan P, const void* q, const
   MOD_REQUIRE(((uintptr_t)o & 15) == 0, MOD_ERR_INPUT, "o must be 16-byte aligned");
   cudaStream_t s = as_stream(stream);
   const int D = P->L.head_dim, BN = P->L.block;
-  if (use_pair2_kernel(P)) {
-    st = launch_pair2(P, q, k, v, row_ptr, col_idx, o, lse, s);
-  } else if (use_dual_kernel()) {
-    if (D == 128 && BN == 128) st = launch_dual<128, 128>(P, q, k, v, row_ptr, col_idx, o, lse, s);
-    else if (D == 64 && BN == 128) st = launch_dual<64, 128>(P, q, k, v, row_ptr, col_idx, o, lse, s);
-    else if (D == 128 && BN == 64) st = launch_dual<128, 64>(P, q, k, v, row_ptr, col_idx, o, lse, s);
-    else st = launch_dual<64, 64>(P, q, k, v, row_ptr, col_idx, o, lse, s);
-  } else if (use_pair_kernel(P)) st = D == 128 ? launch_pair<128>(P, q, k, v, row_ptr, col_idx, o, lse, s)
-                                        : launch_pair<64>(P, q, k, v, row_ptr, col_idx, o, lse, s);
-  else if (D == 128 && BN == 128) st = launch<128, 128>(P, q, k, v, row_ptr, col_idx, o, lse, s);
-  else if (D == 64 && BN == 128) st = launch<64, 128>(P, q, k, v, row_ptr, col_idx, o, lse, s);
-  else if (D == 128 && BN == 64) st = launch<128, 64>(P, q, k, v, row_ptr, col_idx, o, lse, s);
-  else st = launch<64, 64>(P, q, k, v, row_ptr, col_idx, o, lse, s);
+  switch (effective_kernel(P)) {
+    case MOD_ATTN_PAIR2:
+      st = launch_pair2(P, q, k, v, row_ptr, col_idx, o, lse, s);
+      break;
+    case MOD_ATTN_PAIR:
+      st = D == 128 ? launch_pair<128>(P, q, k, v, row_ptr, col_idx, o, lse, s)
+                    : launch_pair<64>(P, q, k, v, row_ptr, col_idx, o, lse, s);
+      break;
+    case MOD_ATTN_SPLITKV:
+      if (D == 128 && BN == 128) st = launch_split<128, 128>(P, q, k, v, row_ptr, col_idx, o, lse, s);
+      else if (D == 64 && BN == 128) st = launch_split<64, 128>(P, q, k, v, row_ptr, col_idx, o, lse, s);
+      else if (D == 128 && BN == 64) st = launch_split<128, 64>(P, q, k, v, row_ptr, col_idx, o, lse, s);
+      else st = launch_split<64, 64>(P, q, k, v, row_ptr, col_idx, o, lse, s);
+      break;
+    default:
+      if (D == 128 && BN == 128) st = launch_default<128, 128>(P, q, k, v, row_ptr, col_idx, o, lse, s);
+      else if (D == 64 && BN == 128) st = launch_default<64, 128>(P, q, k, v, row_ptr, col_idx, o, lse, s);
+      else if (D == 128 && BN == 64) st = launch_default<128, 64>(P, q, k, v, row_ptr, col_idx, o, lse, s);
+      else st = launch_default<64, 64>(P, q, k, v, row_ptr, col_idx, o, lse, s);
+  }
   if (st == MOD_OK) mod_note_launches(1);
   return st;
 }

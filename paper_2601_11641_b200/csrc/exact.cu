@@ -1,5 +1,6 @@
 // exact.cu -- mod_collect_exact_sparsity: the paper's own block statistic (§4.1 Eq. 2,
-// P:204-206) on the GPU, in informativeness polarity U = 1 - S (reading Z3):
+// P:204-206) on the GPU, in informativeness polarity U = -S (reading Z3:
+// the paper's Top-K takes the patterns with the SMALLEST fitted S, i.e. the largest fitted -S):
 //     S_ij = (1/|I_i||I_j|) #{(p,q) in I_i x I_j : P_pq < eta},   P_pq = exp(s Q_p.K_q - lse_p)
 // for every block (i,j) of the CSR list.  lse_p is the log-sum-exp of the attention that produced
 // the map: the dense warm-up attention (all-ones list, t = m-1, m; Alg. 1) or the sparse
@@ -152,7 +153,7 @@ __global__ void __launch_bounds__(320, 1)
       named_bar_sync(1 + g, 128);
       if (quarter == 0 && lane == 0) {
         const int tot = red[g][it & 1][0] + red[g][it & 1][1] + red[g][it & 1][2] + red[g][it & 1][3];
-        Urow[jb] = 1.0f - (float)tot / (float)(q_rows * kv_valid);
+        Urow[jb] = -((float)tot / (float)(q_rows * kv_valid));
       }
     }
   }

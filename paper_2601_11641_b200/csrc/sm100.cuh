@@ -42,6 +42,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// try_wait with a suspend-time hint: the waiting warp sleeps until the phase completes (or the hint
+// expires) instead of re-issuing try_wait, so it leaves its sub-partition's issue slots to the others
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAITS_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "@!P1 bra WAITS_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity), "r"(0x100000u)
+      : "memory");
+}
+
 // busy-polling variant (mbarrier.test_wait never suspends the thread): for the single MMA-issuing
 // thread, whose wake-up latency after a phase flip sits on the tensor pipe's critical path
 __device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
@@ -144,6 +159,47 @@ __device__ __forceinline__ void mma_ts_off(uint32_t d_tmem, uint32_t a_tmem, uin
       "r"(a_tmem), "l"(b_base), "r"(idesc), "r"(accumulate), "n"(A_COL), "n"((uint64_t)B_OFF)
       : "memory");
 }
+// Warp-converged forms (the whole warp executes them; elect.sync picks the one issuing lane inside the
+// asm, so ptxas keeps the descriptors in uniform registers and emits no per-MMA election loop):
+// ACC = 1 accumulate, 0 overwrite, -1 runtime flag `acc`.
+template <uint32_t A_OFF, uint32_t B_OFF>
+__device__ __forceinline__ void mma_ss_e(uint32_t d_tmem, uint64_t a_base, uint64_t b_base, uint32_t idesc,
+                                         uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p, e;\n.reg .b64 ad, bd;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "add.s64 ad, %1, %5;\n"
+      "add.s64 bd, %2, %6;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ad, bd, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a_base), "l"(b_base), "r"(idesc), "r"(acc), "n"((uint64_t)A_OFF), "n"((uint64_t)B_OFF)
+      : "memory");
+}
+template <uint32_t A_COL, uint32_t B_OFF>
+__device__ __forceinline__ void mma_ts_e(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_base, uint32_t idesc,
+                                         uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p, e;\n.reg .b64 bd;\n.reg .b32 at;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "add.s32 at, %1, %5;\n"
+      "add.s64 bd, %2, %6;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [at], bd, %3, p;\n}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_base), "r"(idesc), "r"(acc), "n"(A_COL), "n"((uint64_t)B_OFF)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_e(uint64_t* bar) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\nselp.u32 %0, 1, 0, e;\n}\n" : "=r"(pred));
+  return pred != 0;
+}
+
 template <int I, int N, typename F>
 __device__ __forceinline__ void static_for_impl(F&& f) {
   if constexpr (I < N) {
@@ -290,6 +346,34 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
       "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
       : "memory");
 }
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+// tcgen05.ld / st of N consecutive 32-bit columns (N = 16 or a multiple of 32), 32 lanes
+template <int N>
+__device__ __forceinline__ void tmem_ldn(uint32_t taddr, uint32_t* r) {
+  static_assert(N == 16 || N % 32 == 0, "tmem_ldn: N must be 16 or a multiple of 32");
+  if constexpr (N == 16) {
+    tmem_ld16(taddr, *reinterpret_cast<uint32_t(*)[16]>(r));
+  } else {
+#pragma unroll
+    for (int c = 0; c < N / 32; ++c) tmem_ld32(taddr + c * 32, *reinterpret_cast<uint32_t(*)[32]>(r + c * 32));
+  }
+}
+template <int N>
+__device__ __forceinline__ void tmem_stn(uint32_t taddr, const uint32_t* r) {
+  static_assert(N == 16 || N % 32 == 0, "tmem_stn: N must be 16 or a multiple of 32");
+  if constexpr (N == 16) {
+    tmem_st16(taddr, *reinterpret_cast<const uint32_t(*)[16]>(r));
+  } else {
+#pragma unroll
+    for (int c = 0; c < N / 32; ++c) tmem_st32(taddr + c * 32, *reinterpret_cast<const uint32_t(*)[32]>(r + c * 32));
+  }
+}
 __device__ __forceinline__ uint32_t tmem_ld1(uint32_t taddr) {
   uint32_t r;
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
@@ -313,6 +397,18 @@ __device__ __forceinline__ void setmaxnreg_dec() {   // whole warpgroup
 template <uint32_t R>
 __device__ __forceinline__ void setmaxnreg_inc() {   // whole warpgroup
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(R));
+}
+// named barrier that also ORs a predicate over the participating threads (BAR.RED.OR)
+__device__ __forceinline__ bool named_bar_or(uint32_t id, uint32_t nthreads, bool pred) {
+  uint32_t r;
+  asm volatile(
+      "{\n.reg .pred p, q;\nsetp.ne.u32 p, %1, 0;\n"
+      "barrier.cta.red.or.pred q, %2, %3, p;\n"
+      "selp.u32 %0, 1, 0, q;\n}\n"
+      : "=r"(r)
+      : "r"((uint32_t)pred), "r"(id), "r"(nthreads)
+      : "memory");
+  return r != 0;
 }
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -379,10 +475,15 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
       : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
   return d;
 }
-// 2^x for a pair on the FMA/ALU pipes (packed form of ex2_poly)
+// 2^x for a pair on the FMA/ALU pipes (packed form of ex2_poly); callers guarantee x <= 127.
+template <bool kSat = false>
 __device__ __forceinline__ float2 ex2_poly2(float2 x) {
   x.x = fmaxf(x.x, -126.f);
   x.y = fmaxf(x.y, -126.f);
+  if constexpr (kSat) {   // also clamp above so that the exponent add can neither wrap nor overflow:
+    x.x = fminf(x.x, 127.f);   // 2^x saturates near 2^127 (huge, finite) as ex2.approx saturates to
+    x.y = fminf(x.y, 127.f);   // +inf -- callers that detect overflow through a sum rely on it
+  }
   const float2 t = fadd2(x, make_float2(12582912.0f, 12582912.0f));   // 1.5 * 2^23
   const float2 j = fadd2(t, make_float2(-12582912.0f, -12582912.0f));
   const float2 f = ffma2(j, make_float2(-1.f, -1.f), x);

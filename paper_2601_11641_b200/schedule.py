@@ -1,6 +1,6 @@
 """Algorithm 1 of MOD-DiT for one attention layer, driving the C-ABI kernels.
 
-    t = 1..m           full attention (all-ones index lists; FlashAttention-2 in the paper)
+    t = 1..m           full attention: K4 on all-ones index lists (FlashAttention-2 in the paper)
     t = m-1, m         pooled statistics + mixture fit  X^(m-1), X^(m)
     t = m              block-diagonal keep decision; history seeded with W^(m)
     t > m              mask = predict(x_prev, x_curr; t) (Eq. 6/7 + §5.3) -> block-sparse attention
@@ -33,15 +33,11 @@ class ScheduleState:
 class Schedule:
     def __init__(self, plan: Plan, T: int = 50, m: int = 12, dt: int = 10, top_k: int | None = None,
                  select_mode: int | None = None, select_param: float | None = None, stat: str = "pooled",
-                 eta: float = 1e-4, precision: str = "bf16", warmup_attention: str = "k4"):
+                 eta: float = 1e-4, precision: str = "bf16"):
         if not (1 <= m < T) or dt < 1 or m < 2:
             raise ValueError(f"bad schedule T={T} m={m} dt={dt}")
         if stat not in ("pooled", "exact"):
             raise ValueError(f"stat={stat!r} must be 'pooled' or 'exact'")
-        if warmup_attention not in ("k4", "sdpa"):
-            raise ValueError(f"warmup_attention={warmup_attention!r} must be 'k4' or 'sdpa'")
-        if warmup_attention == "sdpa" and stat == "exact":
-            raise ValueError("warmup_attention='sdpa' needs stat='pooled' (the exact statistic needs K4's lse)")
         if precision not in ("bf16", "q8"):
             raise ValueError(f"precision={precision!r} must be 'bf16' or 'q8'")
         if precision == "q8" and stat == "exact":
@@ -51,7 +47,6 @@ class Schedule:
                              "renormalised by the sparse attention's lse (reading Z12)")
         self.P, self.T, self.m, self.dt = plan, T, m, dt
         self.stat, self.eta, self.precision = stat, eta, precision
-        self.warmup_attention = warmup_attention
         self._qbuf = None
         self.sel = dict(top_k=top_k, select_mode=select_mode, select_param=select_param)
         self.state = ScheduleState()
@@ -74,18 +69,7 @@ class Schedule:
             raise ValueError(f"t={t} outside [1, {self.T}]")
         if t <= self.m:
             rp, ci = self.dense_mask()
-            if self.warmup_attention == "sdpa":
-                # the paper runs its full-attention warm-up on a library kernel (FlashAttention-2,
-                # P:458); this option does the same with torch SDPA (cuDNN on B200).  The warm-up
-                # needs no lse with the pooled statistic; l is returned as None.
-                import torch.nn.functional as F
-                o = F.scaled_dot_product_attention(q, k, v, scale=P.scale)
-                if out is not None:
-                    out.copy_(o)
-                    o = out
-                l = None
-            else:
-                o, l = P.block_sparse_attn_fwd(q, k, v, rp, ci, out=out, lse=lse)
+            o, l = P.block_sparse_attn_fwd(q, k, v, rp, ci, out=out, lse=lse)   # K4 on the all-ones list
             if t == self.m - 1:
                 S.W_warm = self._stat(q, k, l, rp, ci)
                 S.x_prev, S.t_prev = P.fit_mixture(S.W_warm), t

@@ -153,27 +153,12 @@ def main():
             dense_total = sum(per_step[t - 1] for t in range(1, M_WARMUP + 1))
             sparse_total = sum(per_step[t - 1] for t in range(M_WARMUP + 1, T_TOTAL + 1))
             all_dense = T_TOTAL * dense_ms
-            # the same schedule with the warm-up on the library dense kernel (as the paper's FA2 warm-up)
-            S2 = Schedule(P, T=T_TOTAL, m=M_WARMUP, dt=DT, top_k=K, warmup_attention="sdpa")
-            warm2 = 0.0
-            for t in range(1, M_WARMUP + 1):
-                qt, kt, vt = syn.family_s(w, step=t, **gen)
-                torch.cuda.synchronize()
-                a, b = ev(), ev()
-                a.record()
-                S2.step(t, qt, kt, vt, out=o)
-                b.record()
-                torch.cuda.synchronize()
-                warm2 += a.elapsed_time(b)
-                del qt, kt, vt
             print(json.dumps({"part": "run", "config": args.config, "T": T_TOTAL, "m": M_WARMUP, "dt": DT,
                               "top_k": K, "block_sparsity": round(sp, 4),
                               "warmup_ms": round(dense_total, 1), "sparse_steps_ms": round(sparse_total, 1),
                               "schedule_total_ms": round(dense_total + sparse_total, 1),
                               "all_dense_cudnn_ms": round(all_dense, 1),
                               "speedup_vs_all_dense": round(all_dense / (dense_total + sparse_total), 2),
-                              "warmup_ms_with_sdpa_warmup": round(warm2, 1),
-                              "speedup_vs_all_dense_with_sdpa_warmup": round(all_dense / (warm2 + sparse_total), 2),
                               "dense_flops_per_step_tflop": round(dense_flops / 1e12, 2),
                               "note": "warm-up steps run our K4 with the all-ones index list plus the two "
                                       "warm-up statistics/fits; one attention layer"}), flush=True)

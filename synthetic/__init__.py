@@ -74,7 +74,7 @@ def family_r(w: Workload, seed: int = SEED_BASE, device="cpu"):
 
 def family_s(w: Workload, seed: int = SEED_BASE, device="cpu", sigma: float = 0.5,
              kappa: float = 1.0, n_random_sinks: int = 2, step: int = 0, head_offset: int = 0,
-             total_heads: int | None = None):
+             total_heads: int | None = None, drift: float = 0.0, steps_total: int = 50):
     """Family S (structured): planted intra-frame, inter-frame and global-column structure.
 
     Q = a_h*phi(y,x) + b_h*psi(f) + c_h*g_h + sigma*eps
@@ -86,6 +86,10 @@ def family_s(w: Workload, seed: int = SEED_BASE, device="cpu", sigma: float = 0.
     ``step`` re-draws only the noise eps (emulates consecutive denoising steps with the same
     structure).  ``head_offset``/``total_heads`` generate the heads [head_offset, head_offset+H) of a
     ``total_heads``-head problem (head-parallel ranks draw exactly the bytes a single GPU would).
+    ``drift`` > 0 makes the pattern strengths evolve over the denoising steps (the piecewise-smooth
+    intensity trajectories of PAPER.md §4.3): with tau = step / steps_total, the spatial,
+    temporal and sink weights of head h become a_h*(1 + d1*tau + d2*tau^2), etc., with per-head
+    (d1, d2) ~ U(-drift, drift) drawn from their own generator (drift = 0 leaves every byte unchanged).
     """
     B, H, N, D = w.batch, w.heads, w.tokens, w.head_dim
     HT = total_heads or H
@@ -117,6 +121,13 @@ def family_s(w: Workload, seed: int = SEED_BASE, device="cpu", sigma: float = 0.
     phi_t[w.prefix_tokens:] = phi.repeat(w.frames, 1)
     psi_t[w.prefix_tokens:] = psi.repeat_interleave(HW, dim=0)
     tok_block = torch.arange(N) // w.block
+    if drift:
+        gd = _gen(seed + 5, "cpu")
+        dco = (torch.rand((HT, 3, 2), generator=gd, dtype=torch.float64) * 2 - 1) * drift
+        tau = step / float(steps_total)
+        fac = 1.0 + dco[..., 0] * tau + dco[..., 1] * tau * tau                 # [HT, 3]: a, b, kappa
+    else:
+        fac = torch.ones((HT, 3), dtype=torch.float64)
     phi_t, psi_t = phi_t.to(dev), psi_t.to(dev)
     q = torch.empty((B, H, N, D), dtype=torch.bfloat16, device=dev)
     k = torch.empty_like(q)
@@ -124,13 +135,15 @@ def family_s(w: Workload, seed: int = SEED_BASE, device="cpu", sigma: float = 0.
         h = head_offset + hl
         gen_dev = _gen(seed + 1 + 1000 * step + 7919 * h, dev)
         a, b, c = (float(x) for x in abc[h])
+        a, b = a * float(fac[h, 0]), b * float(fac[h, 1])
+        kap = kappa * float(fac[h, 2])
         ghh = gh[h].to(dev)
         sinks_tok = sink_mask[h][tok_block].to(dev).float().unsqueeze(1)          # [N, 1]
         for bb in range(B):
             eq = torch.randn((N, D), generator=gen_dev, device=dev)
             ek = torch.randn((N, D), generator=gen_dev, device=dev)
             qh = a * phi_t + b * psi_t + c * ghh + sigma * eq
-            kh = a * phi_t + b * psi_t + kappa * sinks_tok * ghh + sigma * ek
+            kh = a * phi_t + b * psi_t + kap * sinks_tok * ghh + sigma * ek
             if w.prefix_tokens:
                 qh[: w.prefix_tokens] = torch.randn((w.prefix_tokens, D), generator=gen_dev, device=dev)
                 kh[: w.prefix_tokens] = torch.randn((w.prefix_tokens, D), generator=gen_dev, device=dev)

@@ -1,7 +1,7 @@
-"""K4 kernel variants against the fp64 oracle: the one-block-per-CTA kernel (default), the
-paired-query-block kernel (MOD_ATTN_KERNEL=pair), the two-CTAs-per-SM
-single-chain kernel (MOD_ATTN_KERNEL=dual) and the CTA-pair kernel with M = 256 cta_group::2 MMAs over
-the union of two rows' lists (MOD_ATTN_KERNEL=pair2; D = 128 only, other shapes fall back).
+"""K4 kernel schedules (Plan(attn_kernel=...), include/moddit.h mod_attn_kernel) against the fp64 oracle:
+the default one-softmax-group kernel, the round-1 split-KV kernel ("splitkv"), the paired-query-block
+kernel ("pair") and the CTA-pair kernel with M = 256 cta_group::2 MMAs over the union of
+two rows' lists ("pair2"; D = 128 only, other shapes run the default).
 
 The pair kernel walks the merged index list of query blocks 2p and 2p+1 and shares each K/V tile
 between them, so its masks are chosen to exercise every shape of that merge: lists that coincide,
@@ -31,9 +31,11 @@ def M():
     return m
 
 
-@pytest.fixture(params=["pair", "single", "dual", "pair2"])
-def kernel(request, monkeypatch):
-    monkeypatch.setenv("MOD_ATTN_KERNEL", request.param)
+KERNELS = ["default", "splitkv", "pair", "pair2"]
+
+
+@pytest.fixture(params=KERNELS)
+def kernel(request):
     return request.param
 
 
@@ -94,7 +96,7 @@ def _adversarial(L, heads, seed):
 @pytest.mark.parametrize("w", [ODD, COG_SMALL, SMALL_PREFIX], ids=lambda w: w.name)
 def test_pair_merge_cases(M, kernel, w):
     L = olayout(w)
-    P = M.Plan(w)
+    P = M.Plan(w, attn_kernel=kernel)
     q, k, v = syn.family_r(w, seed=707, device="cuda")
     masks = _adversarial(L, w.heads, 3)
     rp, ci = masks_to_csr(masks)
@@ -107,7 +109,7 @@ def test_pair_merge_cases(M, kernel, w):
 def test_pair_random_density(M, kernel, density):
     w = ODD
     L = olayout(w)
-    P = M.Plan(w)
+    P = M.Plan(w, attn_kernel=kernel)
     q, k, v = syn.family_r(w, seed=708, device="cuda")
     rng = np.random.default_rng(9)
     masks = rng.random((1, w.heads, L.n, L.n)) < density
@@ -117,11 +119,10 @@ def test_pair_random_density(M, kernel, density):
     _check(o, lse, masks, q, k, v, L)
 
 
-def test_pair_and_single_agree_on_structured_masks(M, monkeypatch):
-    """Both variants on MOD-DiT pattern masks at a CogVideoX-like shape (D=64, text prefix)."""
+def test_variants_agree_on_structured_masks(M):
+    """Every schedule on MOD-DiT pattern masks at a CogVideoX-like shape (D=64, text prefix)."""
     w = COG_SMALL
     L = olayout(w)
-    P = M.Plan(w)
     q, k, v = syn.family_s(w, device="cuda")
     rng = np.random.default_rng(12)
     masks = np.zeros((1, w.heads, L.n, L.n), dtype=bool)
@@ -129,24 +130,20 @@ def test_pair_and_single_agree_on_structured_masks(M, monkeypatch):
         sel = O.select_patterns(rng.standard_normal(3 * L.n - 1), L.n, O.SELECT_TOPK, 12)
         masks[0, h] = O.block_mask(sel, rng.random(L.frames) < 0.7, L, True)
     rp, ci = masks_to_csr(masks)
-    res = {}
-    for kern in ("pair", "single", "dual"):
-        monkeypatch.setenv("MOD_ATTN_KERNEL", kern)
-        res[kern] = P.block_sparse_attn_fwd(q, k, v, rp, ci)
+    res = {kern: M.Plan(w, attn_kernel=kern).block_sparse_attn_fwd(q, k, v, rp, ci) for kern in KERNELS}
     torch.cuda.synchronize()
     for kern in res:
         _check(*res[kern], masks, q, k, v, L)
     # different accumulation orders (split-KV merge vs one accumulator): close, not bitwise
-    assert (res["pair"][0].float() - res["single"][0].float()).abs().max().item() <= 2e-2
-    assert (res["dual"][0].float() - res["single"][0].float()).abs().max().item() <= 2e-2
+    for kern in res:
+        assert (res[kern][0].float() - res["default"][0].float()).abs().max().item() <= 2e-2
 
 
-@pytest.mark.parametrize("kern", ["pair", "dual"])
-def test_variant_deterministic(M, monkeypatch, kern):
-    monkeypatch.setenv("MOD_ATTN_KERNEL", kern)
+@pytest.mark.parametrize("kern", KERNELS)
+def test_variant_deterministic(M, kern):
     w = COG_SMALL
     L = olayout(w)
-    P = M.Plan(w)
+    P = M.Plan(w, attn_kernel=kern)
     q, k, v = syn.family_r(w, device="cuda")
     masks = _adversarial(L, w.heads, 4)
     rp, ci = masks_to_csr(masks)
@@ -156,16 +153,39 @@ def test_variant_deterministic(M, monkeypatch, kern):
     assert torch.equal(o1, o2) and torch.equal(l1, l2)
 
 
-@pytest.mark.parametrize("w", [syn.TINY], ids=lambda w: w.name)
-def test_dual_block64(M, monkeypatch, w):
-    """The dual kernel also serves 64-token blocks (the tiny config, D = 64)."""
-    monkeypatch.setenv("MOD_ATTN_KERNEL", "dual")
+@pytest.mark.parametrize("kern", ["default", "splitkv"])
+@pytest.mark.parametrize("w", [syn.TINY, syn.Workload("b64-d128", 1, 2, 128, 0, 2, 10, 13, 64)], ids=lambda w: w.name)
+def test_block64(M, kern, w):
+    """64-token blocks (the tiny config, D = 64; and D = 128): more S buffers, half-width softmax rows."""
     L = olayout(w)
-    P = M.Plan(w)
+    P = M.Plan(w, attn_kernel=kern)
     q, k, v = syn.family_r(w, seed=709, device="cuda")
     rng = np.random.default_rng(10)
     masks = rng.random((1, w.heads, L.n, L.n)) < 0.5
     masks[0, 0, 1] = False
+    rp, ci = masks_to_csr(masks)
+    o, lse = P.block_sparse_attn_fwd(q, k, v, rp, ci)
+    torch.cuda.synchronize()
+    _check(o, lse, masks, q, k, v, L)
+
+
+@pytest.mark.parametrize("kern", KERNELS)
+def test_row_maximum_jumps(M, kern):
+    """Key blocks scaled by 1..60 in list order make the row maximum jump by up to ~100 (log2 units)
+    between blocks -- beyond the default kernel's lazy reference bound (2^20), so its exchange / redo /
+    O-rescale path runs -- and also fall back to small values afterwards (stale reference max)."""
+    w = ODD
+    L = olayout(w)
+    P = M.Plan(w, attn_kernel=kern)
+    q, k, v = syn.family_r(w, seed=711, device="cuda")
+    k = k.clone()
+    scales = [1.0, 3.0, 12.0, 0.5, 25.0, 60.0, 2.0, 40.0, 1.0]
+    for j in range(L.n):
+        lo, hi = L.block_range(j)
+        k[:, :, lo:hi] = (k[:, :, lo:hi].float() * scales[j % len(scales)]).to(torch.bfloat16)
+    rng = np.random.default_rng(13)
+    masks = rng.random((1, w.heads, L.n, L.n)) < 0.7
+    masks[0, 0, 0] = True
     rp, ci = masks_to_csr(masks)
     o, lse = P.block_sparse_attn_fwd(q, k, v, rp, ci)
     torch.cuda.synchronize()

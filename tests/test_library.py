@@ -51,7 +51,7 @@ def test_version_and_error_string_without_gpu():
     # invalid layout is rejected on the host before any device work
     h = ctypes.c_void_p()
     st = m.lib.mod_plan_create(ctypes.byref(ModLayout(1, 1, 96, 0, 1, 1, 1, 128)),
-                               ctypes.byref(ModConfig(1e-8, 0.0, 1, 0, 0.0, 0, 1, 1, 0.0)), 0, ctypes.byref(h))
+                               ctypes.byref(ModConfig(1e-8, 0.0, 1, 0, 0.0, 0, 1, 1, 0.0, 0)), 0, ctypes.byref(h))
     assert st == 2 and b"head_dim=96" in m.lib.mod_last_error()
 
 

@@ -138,3 +138,27 @@ def test_mask_spec_examples():
     m[0, 0] = m[1, 2] = m[3, 1] = True
     assert 1 - m.sum() / 16 == 0.8125                            # S:366 sparsity ratio
     assert L4.n == 4
+
+
+def test_exact_polarity_is_the_papers_ascending_topk_on_fit_of_S():
+    """Reading Z3 with U = -S (EXACT statistic): the descending Top-K on fit(U) must be exactly the
+    paper's literal rule, "Top-K ... in ascending order" of the intensities fitted to S (§5.3),
+    ties by pattern id.  (U = 1 - S would add the per-family offset fit(J) -- C: n/(3n-1),
+    D: (2n-1)/(3n-1), App. Z.5 -- and select different patterns, which this test also shows.)"""
+    L = O.make_layout(1, 1, 8, 0, 3, 4, 4, 4)                # n = 12, F = 3
+    n = L.n
+    rng = np.random.default_rng(21)
+    differs = 0
+    for trial in range(6):
+        S = rng.random((1, 1, n, n))
+        xS = O.fit_mixture(S, L)[0, 0]
+        xU = O.fit_mixture(O.informativeness_from_sparsity(S), L)[0, 0]
+        assert np.array_equal(xU, -xS)                        # the solve is odd in its right-hand side
+        pool = 3 * n - 1
+        for K in (1, 5, 8, 20):
+            literal = np.zeros(pool, dtype=bool)
+            literal[np.lexsort((np.arange(pool), xS[:pool]))[:K]] = True   # ascending on fit(S), ties by id
+            assert np.array_equal(O.select_patterns(O.pattern_keys(xU, L), n, O.SELECT_TOPK, K), literal)
+            x1 = O.fit_mixture(1.0 - S, L)[0, 0]
+            differs += not np.array_equal(O.select_patterns(O.pattern_keys(x1, L), n, O.SELECT_TOPK, K), literal)
+    assert differs > 0

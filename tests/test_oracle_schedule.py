@@ -32,3 +32,23 @@ def test_first_window_uses_warmup_pair():
         sch.step(t, q, k, v, compute_attention=False)
     assert (sch.t_prev, sch.t_curr) == (11, 12)   # spacing 1 in the first window (reading Z10)
     assert sch.keep.shape == (1, 2, 4)
+
+
+def test_drifting_family_s_moves_the_fitted_intensities():
+    """synthetic.family_s(drift>0) gives the oracle pipeline a real trend over denoising steps:
+    the pooled-statistic fits move far more across t than with noise-only steps, and drift = 0 is
+    byte-identical to the plain generator."""
+    import synthetic as syn
+    w = syn.TINY
+    L = O.make_layout(1, 2, 64, 0, 4, 8, 8, 64)
+    assert all(np.array_equal(a.float().numpy(), b.float().numpy())
+               for a, b in zip(syn.family_s(w, step=5), syn.family_s(w, step=5, drift=0.0)))
+
+    def spread(drift):
+        xs = []
+        for t in (13, 25, 37, 49):
+            q, k, _ = syn.family_s(w, step=t, drift=drift)
+            xs.append(O.fit_mixture(O.pooled_block_stats(q, k, L), L))
+        xs = np.stack(xs)
+        return float(np.abs(xs[-1] - xs[0]).mean())
+    assert spread(0.8) > 2.0 * spread(0.0)

@@ -123,3 +123,93 @@ def test_masked_exact_sparsity_rows_match_the_whole_map():
         assert np.allclose(row[~np.isnan(row)], Sm[0, 1, i][~np.isnan(row)], atol=0)
         if m[0, 1, i].any():
             assert np.allclose(lse_i, lse[0, 1, lo:hi], atol=1e-12)
+
+
+# ------------------------------------------------------------------------------------------------
+# Brute-force pins for O2' (Eq. 2, on the POST-softmax map of Alg. 1 line 5):
+# pure-Python loops over single tokens (math.exp, explicit per-row normalisation, strict "<"),
+# independent of the numpy code in oracle/stats.py.  A dropped row normalisation, a "<=" for "<",
+# a transposed operand or a mask applied before/after the normalisation fails one of them.
+
+def _bf_row_probs(qrow, krows, s, allowed):
+    """softmax over the allowed keys of one query row, by explicit loops."""
+    logits = [s * sum(a * b for a, b in zip(qrow, kr)) if ok else None for kr, ok in zip(krows, allowed)]
+    mx = max(x for x in logits if x is not None)
+    e = [math.exp(x - mx) if x is not None else None for x in logits]
+    z = sum(x for x in e if x is not None)
+    return [x / z if x is not None else None for x in e], mx + math.log(z)
+
+
+def _bf_sparsity(q, k, L, eta, block_mask=None):
+    """Eq. 2 by enumeration: S_ij = #{(p,q) in I_i x I_j : P_pq < eta} / (|I_i||I_j|)."""
+    B, H, N, D = q.shape
+    s = 1.0 / math.sqrt(D)
+    S = np.full((B, H, L.n, L.n), np.nan)
+    lse = np.zeros((B, H, N))
+    blk = [p // L.block for p in range(N)]
+    for b in range(B):
+        for h in range(H):
+            cnt = np.zeros((L.n, L.n))
+            for p in range(N):
+                allowed = [True] * N if block_mask is None else [bool(block_mask[b, h, blk[p], blk[t]]) for t in range(N)]
+                P, lse[b, h, p] = _bf_row_probs(q[b, h, p], k[b, h], s, allowed)
+                for t in range(N):
+                    if P[t] is not None and P[t] < eta:
+                        cnt[blk[p], blk[t]] += 1
+            for i in range(L.n):
+                for j in range(L.n):
+                    if block_mask is None or block_mask[b, h, i, j]:
+                        S[b, h, i, j] = cnt[i, j] / (L.block_size(i) * L.block_size(j))
+    return S, lse
+
+
+def test_exact_sparsity_brute_force_ragged():
+    L = O.make_layout(1, 2, 4, 3, 2, 2, 5, 4)       # N = 23: prefix block + ragged last block (size 3)
+    rng = np.random.default_rng(11)
+    q = rng.standard_normal((1, 2, L.N, 4)) * 2.5
+    k = rng.standard_normal((1, 2, L.N, 4)) * 2.5
+    for eta in (1e-3, 2e-2, 0.05):
+        S_bf, _ = _bf_sparsity(q, k, L, eta)
+        assert np.allclose(O.exact_sparsity(q, k, L, eta), S_bf, atol=1e-15, rtol=0)
+        assert 0 < np.nanmean(S_bf) < 1                 # the case is not degenerate
+
+
+def test_exact_sparsity_masked_brute_force_ragged():
+    L = O.make_layout(1, 2, 4, 3, 2, 2, 5, 4)
+    rng = np.random.default_rng(12)
+    q = rng.standard_normal((1, 2, L.N, 4)) * 2.5
+    k = rng.standard_normal((1, 2, L.N, 4)) * 2.5
+    m = rng.random((1, 2, L.n, L.n)) < 0.5
+    m[..., np.arange(L.n), np.arange(L.n)] = True
+    S_bf, lse_bf = _bf_sparsity(q, k, L, 2e-2, m)
+    Sm, lse = O.exact_sparsity_masked(q, k, m, L, 2e-2)
+    assert np.array_equal(np.isnan(Sm), np.isnan(S_bf))
+    assert np.allclose(Sm[~np.isnan(Sm)], S_bf[~np.isnan(S_bf)], atol=1e-15, rtol=0)
+    assert np.allclose(lse, lse_bf, atol=1e-12)
+    rows = O.exact_sparsity_masked_rows(q, k, m[0, 1], L, 0, 1, range(L.n), 2e-2)
+    for i, (row, lse_i) in rows.items():
+        ok = ~np.isnan(S_bf[0, 1, i])
+        assert np.array_equal(np.isnan(row), ~ok)
+        assert np.allclose(row[ok], S_bf[0, 1, i][ok], atol=1e-15, rtol=0)
+
+
+def test_exact_sparsity_strict_threshold_on_exact_probabilities():
+    """Q = 0 makes every post-softmax row uniform: P = 1/N exactly when N is a power of two.
+    eta = 1/N must count nothing (strict "<") and the next double up must count everything;
+    an unnormalised map (P = 1) would count nothing for both."""
+    L = O.make_layout(1, 1, 4, 0, 2, 4, 4, 8)            # N = 32, n = 4
+    q = np.zeros((1, 1, 32, 4))
+    k = np.random.default_rng(13).standard_normal((1, 1, 32, 4))
+    eta = 1.0 / 32
+    assert np.all(O.exact_sparsity(q, k, L, eta) == 0.0)
+    assert np.all(O.exact_sparsity(q, k, L, np.nextafter(eta, 1.0)) == 1.0)
+    # masked form: two selected key blocks of 8 -> P = 1/16 exactly over the selection
+    m = np.zeros((1, 1, L.n, L.n), dtype=bool)
+    m[0, 0, :, 1] = m[0, 0, :, 3] = True
+    Sm, lse = O.exact_sparsity_masked(q, k, m, L, 1.0 / 16)
+    assert np.all(Sm[m] == 0.0) and np.all(np.isnan(Sm[~m]))
+    Sm, _ = O.exact_sparsity_masked(q, k, m, L, np.nextafter(1.0 / 16, 1.0))
+    assert np.all(Sm[m] == 1.0)
+    assert np.allclose(lse, math.log(16), atol=1e-15)
+    rows = O.exact_sparsity_masked_rows(q, k, m[0, 0], L, 0, 0, range(L.n), 1.0 / 16)
+    assert all(np.all(r[~np.isnan(r)] == 0.0) for r, _ in rows.values())
