@@ -341,25 +341,25 @@ __global__ void __launch_bounds__(320, 1)
 // ================================================================================================
 // Default K4 schedule (MOD_ATTN_DEFAULT): ONE softmax group of 8 warps, NS S buffers ahead of it.
 //   warp 0      TMA producer (as above): Q once; K_j into ring slot j % NS, V_j into slot j % 2.
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer:  S_0 .. S_{NS-1}, then per j
+//   warp 1      TMEM allocator + tcgen05.mma issuer:  S_0 .. S_{NS-1}, then per j
 //                  [wait P_j, V_j] PV_j -> O      [wait K_{j+NS}] S_{j+NS} -> S[j % NS]
 //               so S_{j+1} .. S_{j+NS-1} and PV_{j-1} are queued while the softmax works on S_j: the
 //               tensor pipe has 2(NS-1) MMA groups (2048 cycles at NS = 3) of work between S_j and PV_j.
-//   warps 2..   softmax, SPLIT warps per SM sub-partition (4 at 128-key blocks, 2 at 64): warp (quarter q,
-//               part h) owns rows [32q, 32q+32) (its TMEM lane quarter) and key columns [32h, 32h+32) of
-//               every block, so each thread exponentiates 32 scores per block, the SPLIT warps of a
-//               sub-partition hide each other's MUFU / FMA latencies, and they share one running max
-//               and one O (whose D columns they split for the rare rescale and the epilogue).
+//   warps 2..9  softmax, two INDEPENDENT warps per SM sub-partition: warp (quarter q, half h) owns the 16
+//               full rows [32q + 16h, +16) of the tile.  Its TMEM accesses use the .16x32bx2 shape, so
+//               thread t holds row 32q + 16h + t % 16 and the column half t / 16 of every S block (and of O):
+//               the two halves of a row sit in lanes t and t ^ 16 of the SAME warp, and the two warps of a
+//               sub-partition share nothing -- no named barrier per block, so they drift out of phase and
+//               one's loads / stores / waits overlap the other's exponentials (MUFU-bound).
 //               The running max is NOT recomputed per block: the scores are exponentiated against the
 //               current reference max m and the half-row sum tells whether any score exceeded m by
 //               more than 20 (log2 units: p <= sum <= 2^20 -- far from fp32 overflow, exact in the
 //               bf16 P and fp32 l / O that follow).  Only then (first block, or a jump of the row
-//               maximum) do the two warps exchange half-row maxima, redo the block against the new m
-//               and rescale l and O -- the online softmax with a lazily updated reference, which is
-//               exact for any reference (the same result up to rounding).
-//               One named barrier per block among the SPLIT warps of a sub-partition exchanges the
-//               overflow flags and orders all their S loads before any P store (P_j is packed bf16
-//               over the first BN/2 columns of S_j's buffer, the TS operand of PV_j).
+//               maximum) do the two lanes of a row exchange half-row maxima (shuffle), redo the block
+//               against the new m and rescale l and this warp's 16 rows of O -- the online softmax with a
+//               lazily updated reference, which is exact for any reference (same result up to
+//               rounding).  P_j is packed bf16 over the first BN/2 columns of S_j's buffer (the TS operand
+//               of PV_j); the warp's own S loads complete (tcgen05.wait::ld) before its P stores.
 // TMEM: S[b] at [b BN, (b+1) BN) for b < NS, O after them (NS = 3 at D = BN = 128: 512 columns).
 #ifndef K4_WAIT
 #define K4_WAIT mbar_wait_sleep   // producer / MMA-issuer waits (the softmax warps poll)
@@ -369,28 +369,34 @@ struct Attn1Cfg {
   static constexpr int BM = 128;
   static constexpr int NS = (512 - D) / BN > 7 ? 7 : (512 - D) / BN;
   static constexpr int VSTAGES = 2;
-#ifndef K4_SPLIT
-#define K4_SPLIT 2
-#endif
-  static constexpr int SPLIT = BN == 128 ? K4_SPLIT : 2;   // softmax warps per SM sub-partition (row set)
-  static constexpr int COLS = BN / SPLIT;             // score columns per softmax warp (32)
-  static constexpr int OCOLS = D / SPLIT;             // O columns per softmax warp (rescale, epilogue)
+  static constexpr int COLS = BN / 2;                 // score columns per thread (half a row)
+  static constexpr int OCOLS = D / 2;                 // O columns per thread (rescale, epilogue)
   static constexpr int Q_BOX = BM * 128, KV_BOX = BN * 128, NATOM = D / 64;
   static constexpr int Q_BYTES = Q_BOX * NATOM, KV_BYTES = KV_BOX * NATOM;
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + Q_BYTES;
   static constexpr int OFF_V = OFF_K + NS * KV_BYTES;
   static constexpr int OFF_BAR = OFF_V + VSTAGES * KV_BYTES;
-  // q_full, k_full[NS], v_full[2], s_full[NS], p_full[NS], o_done[2]
-  static constexpr int NUM_BARS = 1 + NS + VSTAGES + NS + NS + VSTAGES;
-  static constexpr int OFF_XCH = (OFF_BAR + NUM_BARS * 8 + 16 + 15) / 16 * 16;
-  static constexpr int XCH = 2 * 4 * SPLIT * 32;      // [parity][quarter][part][lane] floats per kind
-  static constexpr int SMEM = OFF_XCH + 3 * XCH * 4;  // kinds: flag, max, l
+  // q_full, k_full[NS], v_full[2], s_full[NS], p_full[NS], o_done[NS] (PV_j commits to o_done[j % NS])
+  static constexpr int NUM_BARS = 1 + NS + VSTAGES + NS + NS + NS;
+  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr int TMEM_O = NS * BN;
   static constexpr uint32_t TMEM_COLS = (NS * BN + D) <= 256 ? 256 : 512;
   static constexpr uint32_t IDESC_S = idesc_bf16_f32(BM, BN, false, false);
   static constexpr uint32_t IDESC_O = idesc_bf16_f32(BM, D, false, true);
-  static constexpr int THREADS = 64 + 128 * SPLIT;    // producer, MMA issuer, 4 x SPLIT softmax warps
+  static constexpr int SOFTMAX_WARPS = 8;
+#ifndef K4_MMA_WARP
+#define K4_MMA_WARP 1
+#endif
+  static constexpr int MMA_WARP = K4_MMA_WARP;        // warp (0 or 1) issuing the MMAs; the other one loads
+#ifndef K4_SPLIT_ISSUE
+#define K4_SPLIT_ISSUE 0
+#endif
+  // 1: the S MMAs are issued by a third warp (warp 10, another SM sub-partition) and the PV MMAs by the MMA
+  // warp, so that the issue stalls of tcgen05.mma (shallow tensor queue) are shared by two sub-partitions
+  static constexpr bool SPLIT_ISSUE = K4_SPLIT_ISSUE != 0;
+  static constexpr int S_WARP = 2 + SOFTMAX_WARPS;
+  static constexpr int THREADS = 64 + 32 * SOFTMAX_WARPS + (SPLIT_ISSUE ? 32 : 0);
 #ifndef K4_EMU
 #define K4_EMU 2
 #endif
@@ -474,8 +480,7 @@ __global__ void __launch_bounds__(Attn1Cfg<D, BN>::THREADS, 1)
   uint64_t* s_full = v_full + C::VSTAGES;
   uint64_t* p_full = s_full + NS;
   uint64_t* o_done = p_full + NS;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + C::VSTAGES);
-  float* xch = reinterpret_cast<float*>(smem + C::OFF_XCH);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + NS);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0 && (smem_u32(smem) & 1023u) != 0) __trap();   // SWIZZLE_128B needs 1024B alignment
@@ -490,24 +495,22 @@ __global__ void __launch_bounds__(Attn1Cfg<D, BN>::THREADS, 1)
     for (int s = 0; s < NS; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&s_full[s], 1);
-      mbar_init(&p_full[s], 4 * C::SPLIT);   // one elected arrival per softmax warp
-    }
-    for (int s = 0; s < C::VSTAGES; ++s) {
-      mbar_init(&v_full[s], 1);
+      mbar_init(&p_full[s], C::SOFTMAX_WARPS);   // one elected arrival per softmax warp
       mbar_init(&o_done[s], 1);
     }
+    for (int s = 0; s < C::VSTAGES; ++s) mbar_init(&v_full[s], 1);
     fence_mbar_init();
   }
 #ifdef MOD_K4_TRACE
   const long long span_c0 = clock64(), span_t0 = gtimer();
 #endif
-  if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  if (warp == C::MMA_WARP) tmem_alloc<C::TMEM_COLS>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
+  if (warp == 1 - C::MMA_WARP) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0 && L > 0) {
       tma_prefetch_desc(&tm_q);
@@ -533,7 +536,7 @@ __global__ void __launch_bounds__(Attn1Cfg<D, BN>::THREADS, 1)
       };
       auto load_v = [&](int j) {
         const int s = j & 1;
-        if (j >= 2) K4_WAIT(&o_done[s], ((j >> 1) - 1) & 1);    // PV_{j-2} has consumed V slot s
+        if (j >= 2) K4_WAIT(&o_done[(j - 2) % NS], ((j - 2) / NS) & 1);   // PV_{j-2} has consumed V slot s
 #ifdef K4_NO_KV
         mbar_arrive(&v_full[s]);
         return;
@@ -551,8 +554,8 @@ __global__ void __launch_bounds__(Attn1Cfg<D, BN>::THREADS, 1)
         if (j + NS < L) load_k(j + NS);
       }
     }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
+  } else if (warp == C::MMA_WARP || (C::SPLIT_ISSUE && warp == C::S_WARP)) {
+    // ------------------------------------------------------------ MMA issuer(s)
     // The whole warp runs this loop converged and elect.sync picks the issuing lane inside each MMA, so
     // descriptors stay in uniform registers and an MMA costs ~2 instructions: this warp shares its SM
     // sub-partition's issue slots with SPLIT softmax warps, and every extra instruction per MMA delays
@@ -590,152 +593,163 @@ __global__ void __launch_bounds__(Attn1Cfg<D, BN>::THREADS, 1)
           constexpr int kk = decltype(kc)::value;
           mma_ts_e<kk * 8, kk * 2048 / 16>(tmem + C::TMEM_O, tmem + b * BN, v_base, C::IDESC_O, kk > 0 ? 1u : acc0);
         });
-        mma_commit_e(&o_done[vs]);         // also releases V slot vs to the producer
+        mma_commit_e(&o_done[b]);          // also releases V slot vs to the producer and (split issue) S buffer b
         K4T(0, 3, j);
-        if (j + NS < L) issue_s(j + NS, bc);   // S buffer b is free once PV_j (issued above, in order) read P_j
+        if constexpr (!C::SPLIT_ISSUE)
+          if (j + NS < L) issue_s(j + NS, bc);   // S buffer b is free once PV_j (issued above, in order) read P_j
         K4T(0, 4, j);
       };
-      static_for<NS>([&](auto bc) {
-        constexpr int b0 = decltype(bc)::value;
-        if (b0 < L) issue_s(b0, bc);
-      });
-      // unrolled over lcm(NS, 2) blocks so that the S buffer and V slot of every step are literals
-      constexpr int U = (NS % 2) ? 2 * NS : NS;
-      for (int j0 = 0; j0 < L; j0 += U) {
-        static_for<U>([&](auto uc) {
-          constexpr int u = decltype(uc)::value;
-          if (j0 + u < L) pv_then_s(j0 + u, std::integral_constant<int, u % NS>{}, std::integral_constant<int, u % 2>{});
+      const bool s_here = !C::SPLIT_ISSUE || warp == C::S_WARP;
+      const bool pv_here = !C::SPLIT_ISSUE || warp == C::MMA_WARP;
+      if (s_here) {
+        static_for<NS>([&](auto bc) {
+          constexpr int b0 = decltype(bc)::value;
+          if (b0 < L) issue_s(b0, bc);
         });
       }
+      if (C::SPLIT_ISSUE && s_here) {
+        // S_j into buffer j % NS once PV_{j-NS} has completed (it read P_{j-NS} from that buffer; MMAs of
+        // different issuing threads are not ordered, so the wait is on the PV commit, not on issue order)
+        for (int j0 = NS; j0 < L; j0 += NS) {
+          static_for<NS>([&](auto bc) {
+            constexpr int b = decltype(bc)::value;
+            const int j = j0 + b;
+            if (j < L) {
+              K4_WAIT(&o_done[b], ((j - NS) / NS) & 1);
+              tc_fence_after();
+              issue_s(j, bc);
+            }
+          });
+        }
+      }
+      if (pv_here) {
+        // unrolled over lcm(NS, 2) blocks so that the S buffer and V slot of every step are literals
+        constexpr int U = (NS % 2) ? 2 * NS : NS;
+        for (int j0 = 0; j0 < L; j0 += U) {
+          static_for<U>([&](auto uc) {
+            constexpr int u = decltype(uc)::value;
+            if (j0 + u < L) pv_then_s(j0 + u, std::integral_constant<int, u % NS>{}, std::integral_constant<int, u % 2>{});
+          });
+        }
+      }
     }
-  } else {
-    // ------------------------------------------------------------ softmax / epilogue (4 x SPLIT warps)
-    constexpr int SPLIT = C::SPLIT, COLS = C::COLS, OCOLS = C::OCOLS, OCH = OCOLS < 32 ? OCOLS : 32;
+  } else if (warp < 2 + C::SOFTMAX_WARPS) {
+    // ------------------------------------------------------------ softmax / epilogue (8 independent warps)
+    constexpr int COLS = C::COLS, OCOLS = C::OCOLS, OCH = OCOLS < 32 ? OCOLS : 32;
+    constexpr unsigned FULL = 0xffffffffu;
     const int quarter = warp & 3;           // TMEM lane quarter this warp may access
-    const int h = (warp - 2) >> 2;          // key-column part of every block (and D part of O)
-    const int row = quarter * 32 + lane;    // query row within the tile
-    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-    const uint32_t bar_id = 1 + quarter;    // named barrier of the SPLIT warps sharing these rows
-    auto X = [&](int kind, int par, int hh) -> float& {
-      return xch[kind * C::XCH + ((par * 4 + quarter) * SPLIT + hh) * 32 + lane];
-    };
-    auto xmax = [&](int kind, int par) {
-      float m = X(kind, par, 0);
-#pragma unroll
-      for (int hh = 1; hh < SPLIT; ++hh) m = fmaxf(m, X(kind, par, hh));
-      return m;
-    };
+    const int h = (warp - 2) >> 2;          // which 16 rows of the quarter
+    const int half = lane >> 4;             // which column half of the row this thread holds
+    const int row = quarter * 32 + h * 16 + (lane & 15);   // query row within the tile
+    const uint32_t lane_off = (uint32_t)(quarter * 32 + h * 16) << 16;
     const int q_row0 = qi * block;
     const int q_rows = min(block, N - q_row0);
-    float m_run = -INFINITY, l_run = 0.f;   // reference max (log2 units, scaled) / this part's row sum
+    float m_run = -INFINITY, l_run = 0.f;   // reference max (log2 units, scaled) / this half-row's sum
     const bool tr = lane == 0;
     const int trole = warp - 1;   // trace role of this softmax warp (1..)
+    int col_next = L > 0 ? cols[0] : 0;   // column index of the next block, loaded one block ahead
 #pragma unroll 1
     for (int j = 0; j < L; ++j) {
       const int b = j % NS;
+      const int col = col_next;
+      if (j + 1 < L) col_next = cols[j + 1];
       if (tr) K4T(trole, 0, j);
       mbar_wait(&s_full[b], (j / NS) & 1);
       if (tr) K4T(trole, 1, j);
       tc_fence_after();
       uint32_t sr[COLS];
-      tmem_ldn<COLS>(tmem + lane_off + b * BN + h * COLS, sr);
+      tmem_ld_rows<COLS, BN / 2>(tmem + lane_off + b * BN, sr);   // columns half * BN/2 + [0, COLS)
       tmem_ld_wait();
       float* s = reinterpret_cast<float*>(sr);
-      const int kv_valid = N - cols[j] * block - h * COLS;   // keys of this part inside the sequence
+      const int kv_valid = N - col * block - half * COLS;   // keys of this half inside the sequence
       if (kv_valid < COLS) {
 #pragma unroll
         for (int c = 0; c < COLS; ++c)
           if (c >= kv_valid) s[c] = -INFINITY;
       }
-      if (j == 0) {   // first block of the list: the exact row maximum (all parts)
-        X(1, 0, h) = row_max<COLS>(s) * scale_log2;
-        named_bar_sync(bar_id, 32 * SPLIT);
-        m_run = xmax(1, 0);                  // finite: every listed block holds >= 1 key
+      if (j == 0) {   // first block of the list: the exact row maximum (both halves)
+        const float mx = row_max<COLS>(s) * scale_log2;
+        m_run = fmaxf(mx, __shfl_xor_sync(FULL, mx, 16));   // finite: every listed block holds >= 1 key
       }
       if (tr) K4T(trole, 2, j);
       uint32_t pk[COLS / 2];
-      float sum = quarter == 1 ? exp_pack<C::EMU1, COLS>(s, scale_log2, m_run, pk)
-                               : exp_pack<C::EMU, COLS>(s, scale_log2, m_run, pk);
+      float sum;
+      if constexpr (C::EMU1 == C::EMU)   // one copy of the loop body (instruction-cache footprint)
+        sum = exp_pack<C::EMU, COLS>(s, scale_log2, m_run, pk);
+      else
+        sum = quarter == C::MMA_WARP ? exp_pack<C::EMU1, COLS>(s, scale_log2, m_run, pk)
+                           : exp_pack<C::EMU, COLS>(s, scale_log2, m_run, pk);
       const bool need = !(sum <= C::OVF);
       if (tr) K4T(trole, 3, j);
-      // any overflow among the SPLIT parts of these 32 rows?  Also orders every part's S_j load
-      // before any P_j store (P_j is packed over the first BN/2 columns of S_j's buffer).
-      const bool any_need = named_bar_or(bar_id, 32 * SPLIT, need);
-      if (tr) K4T(trole, 4, j);
-      if (any_need) {
-        // rare: a row maximum moved up by > 20 (log2): exchange part maxima per row, redo against the new m
-        const int par = j & 1;
-        X(0, par, h) = need ? 1.f : 0.f;
-        X(1, par, h) = row_max<COLS>(s) * scale_log2;
-        named_bar_sync(bar_id, 32 * SPLIT);
-        const bool need_row = xmax(0, par) != 0.f;
-        const float m_new = need_row ? fmaxf(m_run, xmax(1, par)) : m_run;
+      if (__any_sync(FULL, need)) {
+        // rare: a row maximum moved up by > 20 (log2): exchange half-row maxima, redo against the new m
+        const int need_peer = __shfl_xor_sync(FULL, (int)need, 16);   // every lane shuffles (no short-circuit)
+        const bool need_row = need || need_peer != 0;
+        float rmax = row_max<COLS>(s) * scale_log2;
+        rmax = fmaxf(rmax, __shfl_xor_sync(FULL, rmax, 16));
+        const float m_new = need_row ? fmaxf(m_run, rmax) : m_run;
         const float alpha = ex2(m_run - m_new);
         if (need_row) sum = exp_pack<0, COLS>(s, scale_log2, m_new, pk);
         l_run *= alpha;
         m_run = m_new;
-        if (j > 0 && __any_sync(0xffffffffu, alpha < 1.f)) {
-          mbar_wait(&o_done[(j - 1) & 1], ((j - 1) >> 1) & 1);   // PV_{j-1} has written O
+        if (j > 0 && __any_sync(FULL, alpha < 1.f)) {
+          // PV_{j-1} has written O: its slot's previous PV_{j-1-NS} is complete (S_j, committed after
+          // PV_{j-NS}, has been seen) and PV_{j-1+NS} cannot start before this warp's P_{j-1+NS}: unambiguous
+          mbar_wait(&o_done[(j - 1) % NS], ((j - 1) / NS) & 1);
           tc_fence_after();
-          const uint32_t t_o = tmem + lane_off + C::TMEM_O + h * OCOLS;
 #pragma unroll
           for (int c = 0; c < OCOLS / OCH; ++c) {
             uint32_t o[OCH];
-            tmem_ldn<OCH>(t_o + c * OCH, o);
+            tmem_ld_rows<OCH, D / 2>(tmem + lane_off + C::TMEM_O + c * OCH, o);
             tmem_ld_wait();
 #pragma unroll
             for (int e = 0; e < OCH; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-            tmem_stn<OCH>(t_o + c * OCH, o);
+            tmem_st_rows<OCH, D / 2>(tmem + lane_off + C::TMEM_O + c * OCH, o);
           }
         }
-        named_bar_sync(bar_id, 32 * SPLIT);   // the exchange slots of this parity are read by all
       }
+      if (tr) K4T(trole, 4, j);
       l_run += sum;
-      tmem_stn<COLS / 2>(tmem + lane_off + b * BN + h * (COLS / 2), pk);
+      tmem_st_rows<COLS / 2, BN / 4>(tmem + lane_off + b * BN, pk);   // packed P columns half * BN/4 + [0, COLS/2)
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[b]);
       if (tr) K4T(trole, 5, j);
     }
-    // epilogue: l = sum of the parts' sums (they share m), O / l -> bf16 (this warp's D part), lse
-    X(2, 0, h) = l_run;
-    named_bar_sync(bar_id, 32 * SPLIT);
-    float l = 0.f;
-#pragma unroll
-    for (int hh = 0; hh < SPLIT; ++hh) l += X(2, 0, hh);
+    // epilogue: l = sum of the two half-row sums (they share m), O / l -> bf16 (this thread's D half), lse
+    const float l = l_run + __shfl_xor_sync(FULL, l_run, 16);
     const bool valid = row < q_rows;
     const size_t grow = (size_t)bh * N + q_row0 + row;
     if (L > 0) {
-      mbar_wait(&o_done[(L - 1) & 1], ((L - 1) >> 1) & 1);
+      mbar_wait(&o_done[(L - 1) % NS], ((L - 1) / NS) & 1);   // the last PV (its slot's previous PV is complete)
       tc_fence_after();
       const float inv = 1.0f / l;
-      const uint32_t t_o = tmem + lane_off + C::TMEM_O + h * OCOLS;
 #pragma unroll
       for (int c = 0; c < OCOLS / OCH; ++c) {
         uint32_t o[OCH];
-        tmem_ldn<OCH>(t_o + c * OCH, o);
+        tmem_ld_rows<OCH, D / 2>(tmem + lane_off + C::TMEM_O + c * OCH, o);   // columns half * D/2 + c*OCH + [0, OCH)
         tmem_ld_wait();
         uint32_t pkd[OCH / 2];
 #pragma unroll
         for (int e = 0; e < OCH / 2; ++e) pkd[e] = pack_bf16(__uint_as_float(o[2 * e]) * inv, __uint_as_float(o[2 * e + 1]) * inv);
         if (valid) {
-          int4* dst = reinterpret_cast<int4*>(out + grow * D + h * OCOLS + c * OCH);
+          int4* dst = reinterpret_cast<int4*>(out + grow * D + half * OCOLS + c * OCH);
 #pragma unroll
           for (int e = 0; e < OCH / 8; ++e) dst[e] = make_int4(pkd[4 * e], pkd[4 * e + 1], pkd[4 * e + 2], pkd[4 * e + 3]);
         }
       }
-      if (valid && lse && h == 0) lse[grow] = (m_run + __log2f(l)) * 0.69314718055994531f;
+      if (valid && lse && half == 0) lse[grow] = (m_run + __log2f(l)) * 0.69314718055994531f;
     } else if (valid) {
-      int4* dst = reinterpret_cast<int4*>(out + grow * D + h * OCOLS);
+      int4* dst = reinterpret_cast<int4*>(out + grow * D + half * OCOLS);
 #pragma unroll
       for (int e = 0; e < OCOLS / 8; ++e) dst[e] = make_int4(0, 0, 0, 0);
-      if (lse && h == 0) lse[grow] = -INFINITY;
+      if (lse && half == 0) lse[grow] = -INFINITY;
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) {
+  if (warp == C::MMA_WARP) {
     tc_fence_after();
     tmem_dealloc<C::TMEM_COLS>(tmem);
   }

@@ -374,6 +374,66 @@ __device__ __forceinline__ void tmem_stn(uint32_t taddr, const uint32_t* r) {
     for (int c = 0; c < N / 32; ++c) tmem_st32(taddr + c * 32, *reinterpret_cast<const uint32_t(*)[32]>(r + c * 32));
   }
 }
+// .16x32bx2: 16 lanes from taddr's lane, two column halves.  Thread t of the warp gets lane (base + t % 16)
+// and the columns [taddr + (t / 16) * IMM, + 16 or 32) (mapping verified by scripts/micro/tmem_shape_probe.cu),
+// so a warp holds 16 full rows with the two halves of each row in lanes t and t ^ 16.
+template <int IMM>
+__device__ __forceinline__ void tmem_ld16x2_32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x32bx2.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32], %33;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr), "n"(IMM));
+}
+template <int IMM>
+__device__ __forceinline__ void tmem_ld16x2_16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x32bx2.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16], %17;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr), "n"(IMM));
+}
+template <int IMM>
+__device__ __forceinline__ void tmem_st16x2_32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.16x32bx2.x32.b32 [%0], %33, {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]),
+      "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]),
+      "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]), "n"(IMM)
+      : "memory");
+}
+template <int IMM>
+__device__ __forceinline__ void tmem_st16x2_16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.16x32bx2.x16.b32 [%0], %17, {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "n"(IMM)
+      : "memory");
+}
+// N columns per thread (16, 32 or 64) of 16 rows: thread t gets [taddr + (t / 16) * IMM, + N)
+template <int N, int IMM>
+__device__ __forceinline__ void tmem_ld_rows(uint32_t taddr, uint32_t* r) {
+  static_assert(N == 16 || N == 32 || N == 64, "tmem_ld_rows: N must be 16, 32 or 64");
+  if constexpr (N == 16) {
+    tmem_ld16x2_16<IMM>(taddr, *reinterpret_cast<uint32_t(*)[16]>(r));
+  } else {
+#pragma unroll
+    for (int c = 0; c < N / 32; ++c) tmem_ld16x2_32<IMM>(taddr + c * 32, *reinterpret_cast<uint32_t(*)[32]>(r + c * 32));
+  }
+}
+template <int N, int IMM>
+__device__ __forceinline__ void tmem_st_rows(uint32_t taddr, const uint32_t* r) {
+  static_assert(N == 16 || N == 32, "tmem_st_rows: N must be 16 or 32");
+  if constexpr (N == 16)
+    tmem_st16x2_16<IMM>(taddr, *reinterpret_cast<const uint32_t(*)[16]>(r));
+  else
+    tmem_st16x2_32<IMM>(taddr, *reinterpret_cast<const uint32_t(*)[32]>(r));
+}
 __device__ __forceinline__ uint32_t tmem_ld1(uint32_t taddr) {
   uint32_t r;
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
