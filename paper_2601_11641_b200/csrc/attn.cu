@@ -382,21 +382,17 @@ struct Attn1Cfg {
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr int TMEM_O = NS * BN;
   static constexpr uint32_t TMEM_COLS = (NS * BN + D) <= 256 ? 256 : 512;
+  static constexpr int SOFTMAX_WARPS = 8;
+  // MMA issue.  A tcgen05.mma that finds the (shallow) tensor queue full stalls its warp AND slows the
+  // softmax warps of the same SM sub-partition (measured: that sub-partition's softmax falls behind and
+  // paces the CTA), so the issue is spread over two warps on different sub-partitions: warp 0 loads (TMA),
+  // warp 1 issues PV, warp 10 issues S.  (Measured and dropped: one issuer for both, 1580 vs 1444 cycles
+  // per block; S on two alternating warps; pairs of MMAs paced by commits; four issuers over N-halves
+  // with the left S half in the load warp: its waits delay the V loads, 2304 cycles per block.)
+  static constexpr int S_WARP = 2 + SOFTMAX_WARPS;
+  static constexpr int THREADS = 64 + 32 * SOFTMAX_WARPS + 32;
   static constexpr uint32_t IDESC_S = idesc_bf16_f32(BM, BN, false, false);
   static constexpr uint32_t IDESC_O = idesc_bf16_f32(BM, D, false, true);
-  static constexpr int SOFTMAX_WARPS = 8;
-#ifndef K4_MMA_WARP
-#define K4_MMA_WARP 1
-#endif
-  static constexpr int MMA_WARP = K4_MMA_WARP;        // warp (0 or 1) issuing the MMAs; the other one loads
-#ifndef K4_SPLIT_ISSUE
-#define K4_SPLIT_ISSUE 0
-#endif
-  // 1: the S MMAs are issued by a third warp (warp 10, another SM sub-partition) and the PV MMAs by the MMA
-  // warp, so that the issue stalls of tcgen05.mma (shallow tensor queue) are shared by two sub-partitions
-  static constexpr bool SPLIT_ISSUE = K4_SPLIT_ISSUE != 0;
-  static constexpr int S_WARP = 2 + SOFTMAX_WARPS;
-  static constexpr int THREADS = 64 + 32 * SOFTMAX_WARPS + (SPLIT_ISSUE ? 32 : 0);
 #ifndef K4_EMU
 #define K4_EMU 2
 #endif
@@ -404,7 +400,7 @@ struct Attn1Cfg {
 #define K4_EMU1 2
 #endif
   static constexpr int EMU = K4_EMU;                  // pairs of every 8 exponentiated on the FMA pipe
-  static constexpr int EMU1 = K4_EMU1;                // the same on the MMA warp's sub-partition (quarter 1)
+  static constexpr int EMU1 = K4_EMU1;                // the same on the PV warp's sub-partition (quarter 1)
   static constexpr float OVF = 1048576.0f;            // 2^20: half-row sum bound of the lazy reference
 };
 
@@ -504,131 +500,115 @@ __global__ void __launch_bounds__(Attn1Cfg<D, BN>::THREADS, 1)
 #ifdef MOD_K4_TRACE
   const long long span_c0 = clock64(), span_t0 = gtimer();
 #endif
-  if (warp == C::MMA_WARP) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 1 - C::MMA_WARP) {
+  // ---------------------------------------------------------------- loads and MMA issue (warps 0, 1, 10, 11)
+  const uint64_t pol_q = policy_evict_first(), pol_kv = policy_evict_last();
+  auto load_k = [&](int j) {   // one thread
+    const int s = j % NS;
+    unsigned char* dst = smem + C::OFF_K + s * C::KV_BYTES;
+    mbar_arrive_expect_tx(&k_full[s], C::KV_BYTES);
+    const int row = cols[j] * block;
+#pragma unroll
+    for (int a = 0; a < C::NATOM; ++a) tma_load_3d(dst + a * C::KV_BOX, &tm_k, &k_full[s], a * 64, row, bh, pol_kv);
+  };
+  auto load_v = [&](int j) {   // one thread
+    const int s = j & 1;
+    unsigned char* dst = smem + C::OFF_V + s * C::KV_BYTES;
+    mbar_arrive_expect_tx(&v_full[s], C::KV_BYTES);
+    const int row = cols[j] * block;
+#pragma unroll
+    for (int a = 0; a < C::NATOM; ++a) tma_load_3d(dst + a * C::KV_BOX, &tm_v, &v_full[s], a * 64, row, bh, pol_kv);
+  };
+  // S_j = Q K_j^T into S buffer b = j % NS; whole warp, converged (elect.sync inside each MMA keeps the
+  // descriptors in uniform registers)
+  auto issue_s = [&](int j, auto bc) {
+    constexpr int b = decltype(bc)::value;
+    K4_WAIT(&k_full[b], (j / NS) & 1);
+    tc_fence_after();
+    const uint64_t a_base = smem_desc_sw128(smem_u32(smem + C::OFF_Q), 16, 1024);
+    const uint64_t b_base = smem_desc_sw128(smem_u32(smem + C::OFF_K + b * C::KV_BYTES), 16, 1024);
+    // K-major SW128: 32 bytes per K step inside a 128B atom, atoms one box apart (offsets in 16 B)
+    static_for<D / 16>([&](auto kc) {
+      constexpr int kk = decltype(kc)::value;
+      mma_ss_e<((kk / 4) * C::Q_BOX + (kk % 4) * 32) / 16, ((kk / 4) * C::KV_BOX + (kk % 4) * 32) / 16>(
+          tmem + b * BN, a_base, b_base, C::IDESC_S, kk > 0 ? 1u : 0u);
+    });
+    mma_commit_e(&s_full[b]);          // also releases K slot b to the producer
+  };
+  // PV_j: O += P_j V_j with P_j from TMEM (TS form)
+  auto issue_pv = [&](int j, auto bc, auto vc) {
+    constexpr int b = decltype(bc)::value, vs = decltype(vc)::value;
+    K4T(0, 0, j);
+    K4_WAIT(&v_full[vs], (j >> 1) & 1);
+    K4T(0, 1, j);
+    K4_WAIT(&p_full[b], (j / NS) & 1);
+    K4T(0, 2, j);
+    tc_fence_after();
+    // B = V_j: N = D (MN-major, 64-column atoms LBO = KV_BOX apart), K = 16 keys = 2048 bytes
+    const uint64_t v_base = smem_desc_sw128(smem_u32(smem + C::OFF_V + vs * C::KV_BYTES), C::KV_BOX, 1024);
+    const uint32_t acc0 = j > 0 ? 1u : 0u;
+    static_for<BN / 16>([&](auto kc) {
+      constexpr int kk = decltype(kc)::value;
+      mma_ts_e<kk * 8, kk * 2048 / 16>(tmem + C::TMEM_O, tmem + b * BN, v_base, C::IDESC_O, kk > 0 ? 1u : acc0);
+    });
+    mma_commit_e(&o_done[b]);          // also releases V slot vs to the producer
+    K4T(0, 3, j);
+  };
+  constexpr int UPV = (NS % 2) ? 2 * NS : NS;   // PV loops unrolled over lcm(NS, 2): literal slots
+
+  if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0 && L > 0) {
       tma_prefetch_desc(&tm_q);
       tma_prefetch_desc(&tm_k);
       tma_prefetch_desc(&tm_v);
-      const uint64_t pol_q = policy_evict_first(), pol_kv = policy_evict_last();
       mbar_arrive_expect_tx(q_full, C::Q_BYTES);
 #pragma unroll
       for (int a = 0; a < C::NATOM; ++a)
         tma_load_3d(smem + C::OFF_Q + a * C::Q_BOX, &tm_q, q_full, a * 64, qi * block, bh, pol_q);
-      auto load_k = [&](int j) {
-        const int s = j % NS;
-        if (j >= NS) K4_WAIT(&s_full[s], ((j / NS) - 1) & 1);   // S_{j-NS} has consumed K slot s
-#ifdef K4_NO_KV
-        mbar_arrive(&k_full[s]);
-        return;
-#endif
-        unsigned char* dst = smem + C::OFF_K + s * C::KV_BYTES;
-        mbar_arrive_expect_tx(&k_full[s], C::KV_BYTES);
-        const int row = cols[j] * block;
-#pragma unroll
-        for (int a = 0; a < C::NATOM; ++a) tma_load_3d(dst + a * C::KV_BOX, &tm_k, &k_full[s], a * 64, row, bh, pol_kv);
-      };
-      auto load_v = [&](int j) {
-        const int s = j & 1;
-        if (j >= 2) K4_WAIT(&o_done[(j - 2) % NS], ((j - 2) / NS) & 1);   // PV_{j-2} has consumed V slot s
-#ifdef K4_NO_KV
-        mbar_arrive(&v_full[s]);
-        return;
-#endif
-        unsigned char* dst = smem + C::OFF_V + s * C::KV_BYTES;
-        mbar_arrive_expect_tx(&v_full[s], C::KV_BYTES);
-        const int row = cols[j] * block;
-#pragma unroll
-        for (int a = 0; a < C::NATOM; ++a) tma_load_3d(dst + a * C::KV_BOX, &tm_v, &v_full[s], a * 64, row, bh, pol_kv);
-      };
-      // demand order of the MMA warp: K_0 .. K_{NS-1}, then V_j, K_{j+NS} for j = 0, 1, ...
+      // demand order of the MMA warps: K_0 .. K_{NS-1}, then V_j, K_{j+NS} for j = 0, 1, ...
       for (int j = 0; j < NS && j < L; ++j) load_k(j);
       for (int j = 0; j < L; ++j) {
+        if (j >= 2) K4_WAIT(&o_done[(j - 2) % NS], ((j - 2) / NS) & 1);   // PV_{j-2} has consumed V slot j % 2
         load_v(j);
-        if (j + NS < L) load_k(j + NS);
-      }
-    }
-  } else if (warp == C::MMA_WARP || (C::SPLIT_ISSUE && warp == C::S_WARP)) {
-    // ------------------------------------------------------------ MMA issuer(s)
-    // The whole warp runs this loop converged and elect.sync picks the issuing lane inside each MMA, so
-    // descriptors stay in uniform registers and an MMA costs ~2 instructions: this warp shares its SM
-    // sub-partition's issue slots with SPLIT softmax warps, and every extra instruction per MMA delays
-    // the tensor pipe (scripts/micro/mma_probe.cu: 1037 -> 1650 cycles per block with 4 busy neighbours).
-    if (L > 0) {
-      const uint32_t sq = smem_u32(smem + C::OFF_Q);
-      K4_WAIT(q_full, 0);
-      tc_fence_after();
-      const uint64_t a_base = smem_desc_sw128(sq, 16, 1024);
-      auto issue_s = [&](int j, auto bc) {   // bc: compile-time S buffer index j % NS
-        constexpr int b = decltype(bc)::value;
-        K4_WAIT(&k_full[b], (j / NS) & 1);
-        tc_fence_after();
-        const uint64_t b_base = smem_desc_sw128(smem_u32(smem + C::OFF_K + b * C::KV_BYTES), 16, 1024);
-        // K-major SW128: 32 bytes per K step inside a 128B atom, atoms one box apart (offsets in 16 B)
-        static_for<D / 16>([&](auto kc) {
-          constexpr int kk = decltype(kc)::value;
-          mma_ss_e<((kk / 4) * C::Q_BOX + (kk % 4) * 32) / 16, ((kk / 4) * C::KV_BOX + (kk % 4) * 32) / 16>(
-              tmem + b * BN, a_base, b_base, C::IDESC_S, kk > 0 ? 1u : 0u);
-        });
-        mma_commit_e(&s_full[b]);          // also releases K slot b to the producer
-      };
-      auto pv_then_s = [&](int j, auto bc, auto vc) {   // b = j % NS, vs = j % 2 (compile time)
-        constexpr int b = decltype(bc)::value, vs = decltype(vc)::value;
-        K4T(0, 0, j);
-        K4_WAIT(&v_full[vs], (j >> 1) & 1);
-        K4T(0, 1, j);
-        K4_WAIT(&p_full[b], (j / NS) & 1);
-        K4T(0, 2, j);
-        tc_fence_after();
-        const uint64_t v_base = smem_desc_sw128(smem_u32(smem + C::OFF_V + vs * C::KV_BYTES), C::KV_BOX, 1024);
-        const uint32_t acc0 = j > 0 ? 1u : 0u;
-        // B = V_j: N = D (MN-major, 64-column atoms LBO = KV_BOX apart), K = 16 keys = 2048 bytes
-        static_for<BN / 16>([&](auto kc) {
-          constexpr int kk = decltype(kc)::value;
-          mma_ts_e<kk * 8, kk * 2048 / 16>(tmem + C::TMEM_O, tmem + b * BN, v_base, C::IDESC_O, kk > 0 ? 1u : acc0);
-        });
-        mma_commit_e(&o_done[b]);          // also releases V slot vs to the producer and (split issue) S buffer b
-        K4T(0, 3, j);
-        if constexpr (!C::SPLIT_ISSUE)
-          if (j + NS < L) issue_s(j + NS, bc);   // S buffer b is free once PV_j (issued above, in order) read P_j
-        K4T(0, 4, j);
-      };
-      const bool s_here = !C::SPLIT_ISSUE || warp == C::S_WARP;
-      const bool pv_here = !C::SPLIT_ISSUE || warp == C::MMA_WARP;
-      if (s_here) {
-        static_for<NS>([&](auto bc) {
-          constexpr int b0 = decltype(bc)::value;
-          if (b0 < L) issue_s(b0, bc);
-        });
-      }
-      if (C::SPLIT_ISSUE && s_here) {
-        // S_j into buffer j % NS once PV_{j-NS} has completed (it read P_{j-NS} from that buffer; MMAs of
-        // different issuing threads are not ordered, so the wait is on the PV commit, not on issue order)
-        for (int j0 = NS; j0 < L; j0 += NS) {
-          static_for<NS>([&](auto bc) {
-            constexpr int b = decltype(bc)::value;
-            const int j = j0 + b;
-            if (j < L) {
-              K4_WAIT(&o_done[b], ((j - NS) / NS) & 1);
-              tc_fence_after();
-              issue_s(j, bc);
-            }
-          });
+        if (j + NS < L) {
+          K4_WAIT(&s_full[j % NS], (j / NS) & 1);   // S_j has consumed K slot j % NS
+          load_k(j + NS);
         }
       }
-      if (pv_here) {
-        // unrolled over lcm(NS, 2) blocks so that the S buffer and V slot of every step are literals
-        constexpr int U = (NS % 2) ? 2 * NS : NS;
-        for (int j0 = 0; j0 < L; j0 += U) {
-          static_for<U>([&](auto uc) {
+    }
+  } else if (warp == 1 || warp == C::S_WARP) {
+    // ------------------------------------------------------------ MMA issuers
+    if (L > 0) {
+      K4_WAIT(q_full, 0);
+      tc_fence_after();
+      if (warp == 1) {
+        for (int j0 = 0; j0 < L; j0 += UPV) {
+          static_for<UPV>([&](auto uc) {
             constexpr int u = decltype(uc)::value;
-            if (j0 + u < L) pv_then_s(j0 + u, std::integral_constant<int, u % NS>{}, std::integral_constant<int, u % 2>{});
+            if (j0 + u < L) issue_pv(j0 + u, std::integral_constant<int, u % NS>{}, std::integral_constant<int, u % 2>{});
+          });
+        }
+      } else {
+        // S_j into buffer j % NS once PV_{j-NS} has completed (it read P_{j-NS} from that buffer; MMAs of
+        // different issuing threads are not ordered, so the wait is on the PV commit).  Each wait is on
+        // the next phase of its barrier in order, so the parities are unambiguous.
+        for (int j0 = 0; j0 < L; j0 += NS) {
+          static_for<NS>([&](auto uc) {
+            constexpr int u = decltype(uc)::value;
+            const int j = j0 + u;
+            if (j < L) {
+              if (j >= NS) {
+                K4_WAIT(&o_done[u], ((j - NS) / NS) & 1);
+                tc_fence_after();
+              }
+              issue_s(j, uc);
+            }
           });
         }
       }
@@ -677,7 +657,7 @@ __global__ void __launch_bounds__(Attn1Cfg<D, BN>::THREADS, 1)
       if constexpr (C::EMU1 == C::EMU)   // one copy of the loop body (instruction-cache footprint)
         sum = exp_pack<C::EMU, COLS>(s, scale_log2, m_run, pk);
       else
-        sum = quarter == C::MMA_WARP ? exp_pack<C::EMU1, COLS>(s, scale_log2, m_run, pk)
+        sum = quarter == 1 ? exp_pack<C::EMU1, COLS>(s, scale_log2, m_run, pk)
                            : exp_pack<C::EMU, COLS>(s, scale_log2, m_run, pk);
       const bool need = !(sum <= C::OVF);
       if (tr) K4T(trole, 3, j);
@@ -749,7 +729,7 @@ __global__ void __launch_bounds__(Attn1Cfg<D, BN>::THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == C::MMA_WARP) {
+  if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<C::TMEM_COLS>(tmem);
   }
