@@ -99,6 +99,13 @@ typedef struct {
   int32_t attn_kernel;  /* mod_attn_kernel (K4 schedule); 0 = default */
 } mod_config;
 
+/* Which step of the App. B solver chain produced the plan's Gram inverse. */
+typedef enum {
+  MOD_SOLVER_CHOLESKY = 0,  /* SPD elimination without pivoting (the primary method) */
+  MOD_SOLVER_LU = 1,        /* elimination with partial pivoting */
+  MOD_SOLVER_PINV = 2       /* pseudo-inverse: eigenvalues below 1e-6 x max G_ii dropped */
+} mod_solver;
+
 /* Per-call selection override for mod_predict_block_mask (nullable: plan defaults). */
 typedef struct {
   int32_t select_mode;
@@ -112,9 +119,15 @@ typedef struct mod_plan_s* mod_plan;
  *   frame block ranges [a_r,b_r] = [floor((P0+r*HW)/block), floor((P0+(r+1)*HW-1)/block)] (Z5);
  *   the closed-form Gram G = M^T M + lambda*I (App. B, plus counted C^T E, D^T E,
  *   overlapping E^T E) and its inverse after deflating the analytically known null space of M
- *   (DESIGN.md "Fit numerics"): fp64 p x p, p^2*8 bytes of device memory.
- * Returns MOD_ERR_INPUT for a bad layout, MOD_ERR_NUMERICAL if the deflated Gram is not
- * numerically positive definite, MOD_ERR_UNSUPPORTED if `device` is not sm_100. */
+ *   (DESIGN.md "Fit numerics"): fp64, p rows of mod_plan_gram_inverse_ld doubles on the device.
+ *   The inverse follows the App. B chain: Gauss-Jordan without pivoting (Cholesky class:
+ *   accepted when every pivot is positive and the condition estimate max G_ii x max (G^-1)_ii <= 1e7);
+ *   else with partial pivoting (LU class, same acceptance on finite pivots); else the pseudo-inverse
+ *   step -- the eigenvectors whose eigenvalues fall below 1e-6 x max G_ii are found by inverse iteration
+ *   and deflated like the analytic null space (a dependency the analytic list misses, e.g. degenerate
+ *   tiny layouts).
+ * Returns MOD_ERR_INPUT for a bad layout, MOD_ERR_NUMERICAL if the whole chain fails,
+ * MOD_ERR_UNSUPPORTED if `device` is not sm_100. */
 mod_status mod_plan_create(const mod_layout* layout /*host*/, const mod_config* cfg /*host*/, int device,
                            mod_plan* out /*host*/);
 void mod_plan_destroy(mod_plan plan);
@@ -127,8 +140,14 @@ mod_status mod_plan_frame_blocks(mod_plan plan, int32_t* a_b /*host*/);
  * analytic null space (host out).  A min pivot of order lambda flags a dependency the analytic list
  * missed (degenerate tiny layouts); X then carries the undeflated ~cond(G)*eps error. */
 mod_status mod_plan_diagnostics(mod_plan plan, double* min_pivot, int32_t* null_dim);
-/* Device pointer to the fp64 deflated Gram inverse (p x p), for diagnostics. */
+/* Device pointer to the fp64 deflated Gram inverse (p rows, leading dimension mod_plan_gram_inverse_ld
+ * doubles; symmetric), for diagnostics. */
 const double* mod_plan_gram_inverse(mod_plan plan);
+int32_t mod_plan_gram_inverse_ld(mod_plan plan);
+/* mod_solver of the App. B chain step that produced the inverse. */
+int32_t mod_plan_solver(mod_plan plan);
+/* Host wall time of mod_plan_create (milliseconds). */
+double mod_plan_create_ms(mod_plan plan);
 const char* mod_last_error(void);
 const char* mod_version(void);
 /* Name of the K4 kernel instantiation mod_block_sparse_attn_fwd launches for this plan (static string,

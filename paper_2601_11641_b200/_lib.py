@@ -56,6 +56,9 @@ SIGNATURES = {
     "mod_plan_frame_blocks": (I32, [P, C.POINTER(I32)]),
     "mod_plan_diagnostics": (I32, [P, C.POINTER(C.c_double), C.POINTER(I32)]),
     "mod_plan_gram_inverse": (P, [P]),
+    "mod_plan_gram_inverse_ld": (I32, [P]),
+    "mod_plan_solver": (I32, [P]),
+    "mod_plan_create_ms": (C.c_double, [P]),
     "mod_last_error": (C.c_char_p, []),
     "mod_version": (C.c_char_p, []),
     "mod_attn_kernel_name": (C.c_char_p, [P]),

@@ -51,21 +51,28 @@ struct mod_plan_s {
   int* d_frame_ab;              // device [2F]
   int* d_row_frames;            // device [2n]: frames containing block i are [lo, hi] (hi < lo: none)
   float* d_log_sizes;           // device [n]: ln |I_j|
-  double* d_ginv;               // device [p*p] deflated Gram inverse
+  double* d_ginv;               // device [p rows x ginv_ld] deflated Gram inverse (symmetric)
+  int ginv_ld;                  // leading dimension of d_ginv (p rounded up to 32: 256-byte rows)
+  CUtensorMap tm_ginv;          // 2D TMA map over d_ginv: {ld, p} fp64, box {128 columns, 32 rows}
   size_t ws_bytes;
   // workspace carve (byte offsets)
   size_t ws_qbar, ws_kbar, ws_part, ws_r, ws_x, ws_nae, ws_sel, ws_cnt, ws_solve;
-  int proj_tiles;               // row tiles of the projection kernel
+  int proj_tiles, proj_rows;    // row tiles of the projection kernel / map rows per tile (<= 32, in smem)
+  int solve_segs, solve_seg_len; // split-K segments of the X = G'^-1 r stream (fit.cu)
   int sm_count;
-  double min_pivot;             // smallest Gauss-Jordan pivot of the deflated Gram
-  int null_dim;                 // dimension of the deflated (analytic) null space
+  double min_pivot;             // smallest Gauss-Jordan pivot (magnitude) of the accepted inversion
+  int null_dim;                 // dimension of the deflated null space (analytic + numerically found)
+  double cond_est;              // condition estimate of the accepted inversion (max G_ii x max Ginv_ii)
+  int solver;                   // mod_solver that produced d_ginv (App. B chain: Cholesky, LU, pinv)
+  double create_ms;             // host wall time of mod_plan_create
 };
 
 mod_status mod_validate_plan(mod_plan plan);
 
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
-constexpr int kProjRows = 32;    // rows per projection tile (fit / update)
+constexpr int kProjRows = 32;    // max rows per projection tile (fit / update)
+constexpr int kProjSmemFloats = 28672;   // shared-memory map tile of the projection (112 KB)
 constexpr int kMaxBlocks = 2048; // n limit (pattern pool 3n-1 sorted in shared memory)
 
 // ------------------------------------------------------------------------------------------------

@@ -13,42 +13,89 @@
 // Update (Eq. 5, readings Z11/Z12): for every selected block (i,j) of the CSR mask,
 //   hist[i,j] = W[i,j] / sum_{j' selected in row i} W[i,j']   (fp64 sum, rounded once to fp32),
 // unselected entries untouched; then X = fit(hist), x_prev <- x_curr, x_curr <- X.
+#include <algorithm>
+
 #include "common.cuh"
+#include "sm100.cuh"
+
+using namespace sm100;
 
 namespace {
 
+// One CTA per (head, tile of `rows` consecutive map rows).  The tile is a contiguous run of rows * n fp32
+// values of U: its 16-byte-aligned interior is staged in shared memory by ONE bulk copy on the TMA engine
+// (HBM-bound: every map byte is read once; two CTAs per SM overlap one's copy with the other's sums),
+// then the C (diagonal), D (column) and E (frame-square) partial sums of the tile are formed from shared
+// memory in fp64, each in a fixed order (deterministic).
 __global__ void __launch_bounds__(256) project_kernel(const float* __restrict__ U, double* __restrict__ part,
                                                        const int* __restrict__ frame_ab, int n, int F, int p,
-                                                       int tiles) {
+                                                       int tiles, int rows) {
+  extern __shared__ __align__(128) float tile_raw[];
+  __shared__ __align__(8) uint64_t bar;
   const size_t bh = blockIdx.y;
   const int tile = blockIdx.x;
-  const int i0 = tile * kProjRows, i1 = min(i0 + kProjRows, n);
-  const float* Uh = U + bh * (size_t)n * n;
+  const int i0 = tile * rows, i1 = min(i0 + rows, n), R = i1 - i0;
+  const size_t start = (bh * n + i0) * (size_t)n;     // first element of the tile (contiguous rows)
+  const size_t count = (size_t)R * n;
+  const int shift = (int)(start & 3);                 // so that 16-byte global chunks land 16-byte aligned
+  float* t = tile_raw + 4 + shift;                    // t[i * n + j] = U[bh][i0 + i][j]; tile_raw[0..3] pad
+  const float* src = U + start;
+  const size_t head = min(count, (size_t)((4 - shift) & 3));    // scalars before the first aligned chunk
+  const size_t nvec = (count - head) / 4;                       // aligned 16-byte chunks
+  const uint32_t bytes = (uint32_t)(nvec * 16);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && bytes > 0) {
+    mbar_arrive_expect_tx(&bar, bytes);
+    bulk_load(t + head, src + head, bytes, &bar);
+  }
+  for (size_t e = threadIdx.x; e < head; e += blockDim.x) t[e] = src[e];
+  for (size_t e = head + 4 * nvec + threadIdx.x; e < count; e += blockDim.x) t[e] = src[e];
+  if (bytes > 0) mbar_wait(&bar, 0);
+  __syncthreads();
   double* out = part + (bh * tiles + tile) * (size_t)p;
-  const int t = threadIdx.x;
+  const int tid = threadIdx.x;
   // C part: diagonal offset d = k - (n-1); entries (i, i+d) of this tile
-  for (int k = t; k < 2 * n - 1; k += blockDim.x) {
+  // (each sum is formed as four interleaved partial sums over i mod 4 added at the end: a fixed order,
+  // with four independent shared-memory load -> add chains in flight)
+  for (int k = tid; k < 2 * n - 1; k += blockDim.x) {
     const int d = k - (n - 1);
-    double s = 0.0;
-    for (int i = i0; i < i1; ++i) {
-      const int j = i + d;
-      if (j >= 0 && j < n) s += (double)Uh[(size_t)i * n + j];
+    const int ilo = max(0, -(i0 + d)), ihi = min(R, n - (i0 + d));   // rows of the tile with 0 <= i0+i+d < n
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    const float* q = t + i0 + d;   // q[i * (n + 1)] = t[i * n + i0 + i + d]
+    int i = ilo;
+    for (; i + 4 <= ihi; i += 4) {
+      s0 += (double)q[i * (n + 1)];
+      s1 += (double)q[(i + 1) * (n + 1)];
+      s2 += (double)q[(i + 2) * (n + 1)];
+      s3 += (double)q[(i + 3) * (n + 1)];
     }
-    out[k] = s;
+    for (; i < ihi; ++i) s0 += (double)q[i * (n + 1)];
+    out[k] = (s0 + s1) + (s2 + s3);
   }
   // D part: column sums of this tile
-  for (int j = t; j < n; j += blockDim.x) {
-    double s = 0.0;
-    for (int i = i0; i < i1; ++i) s += (double)Uh[(size_t)i * n + j];
-    out[2 * n - 1 + j] = s;
+  for (int j = tid; j < n; j += blockDim.x) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int i = 0;
+    for (; i + 4 <= R; i += 4) {
+      s0 += (double)t[i * n + j];
+      s1 += (double)t[(i + 1) * n + j];
+      s2 += (double)t[(i + 2) * n + j];
+      s3 += (double)t[(i + 3) * n + j];
+    }
+    for (; i < R; ++i) s0 += (double)t[i * n + j];
+    out[2 * n - 1 + j] = (s0 + s1) + (s2 + s3);
   }
   // E part: frame squares intersecting this tile (one warp per frame)
-  const int warp = t / 32, lane = t % 32;
+  const int warp = tid / 32, lane = tid % 32;
   for (int r = warp; r < F; r += blockDim.x / 32) {
     const int a = frame_ab[2 * r], b = frame_ab[2 * r + 1];
     double s = 0.0;
     for (int i = max(a, i0); i <= min(b, i1 - 1); ++i)
-      for (int j = a + lane; j <= b; j += 32) s += (double)Uh[(size_t)i * n + j];
+      for (int j = a + lane; j <= b; j += 32) s += (double)t[(i - i0) * n + j];
     s = warp_sum_d(s);
     if (lane == 0) out[3 * n - 1 + r] = s;
   }
@@ -64,47 +111,143 @@ __global__ void reduce_rhs_kernel(const double* __restrict__ part, double* __res
   r[e] = s;
 }
 
-// X[bh][k] = sum_l G'^-1[k][l] r[bh][l] as a split-K GEMM: CTA (32 rows k, 32 heads, one l segment),
-// 64 threads with 4 x 4 register tiles over shared-memory chunks of 32 l; partial sums go to a
-// [segments, BH, p] buffer that solve_reduce_kernel adds in fixed order (deterministic, no atomics).
-constexpr int SK_SEG = 8, SK_T = 32, SK_L = 32;
-__global__ void __launch_bounds__(64) solve_partial_kernel(const double* __restrict__ Ginv, const double* __restrict__ r,
-                                                           double* __restrict__ part, int p, int BH, int seg_len) {
-  __shared__ double Gs[SK_L][SK_T + 1];   // [l][k]
-  __shared__ double Rs[SK_L][SK_T + 1];   // [l][bh]
-  const int k0 = blockIdx.x * SK_T, b0 = blockIdx.y * SK_T, seg = blockIdx.z;
+// X[bh][k] = sum_l G'^-1[k][l] r[bh][l].  G'^-1 is symmetric (inverse of the SPD deflated Gram), so the
+// sum runs over its ROWS l.  One CTA per (tile of 128 columns k, segment of rows l, chunk of HB heads),
+// one wave over the SMs.  A producer thread streams the segment's 32-row x 128-column boxes of G'^-1
+// (one 32 KB TMA load each, 2D tensor map) through a 3-stage shared-memory ring (~96 KB in flight per SM).  256 consumer threads are register-blocked: thread (column quad, head half, row group) forms
+// 4 columns x HB/2 heads of X from 2 + HB/4 shared-memory vector loads per row (G values and r values,
+// the segment's r staged in shared memory), so the loop is bound by the fp64 FMAs (~62 DFMA/clk/SM on
+// B200, scripts/micro/fp64_bench.cu), about the time of the HBM stream at HB = 24.  The four row groups
+// are added in fixed order through shared memory; split-K partials over segments are added by
+// solve_reduce_kernel in fixed order (deterministic, no atomics).  G'^-1 is read once per call for up to
+// HB heads.
+constexpr int SV_K = 128;                  // columns k per CTA
+constexpr int SV_G = 4;                    // row groups
+constexpr int SV_ROWS = 32;                // rows per ring stage
+constexpr int SV_STAGES = 3;
+constexpr int SV_SMEM_G = SV_STAGES * SV_ROWS * SV_K * 8;   // 96 KB
+constexpr int SV_CONS = (SV_K / 4) * 2 * SV_G;              // 256 consumer threads
+constexpr int SV_THREADS = SV_CONS + 32;
+template <int HB>
+__global__ void __launch_bounds__(SV_THREADS, 1) solve_stream_kernel(const __grid_constant__ CUtensorMap tm, int ld,
+                                                                     const double* __restrict__ r,
+                                                                     double* __restrict__ part, int p, int BH,
+                                                                     int seg_len) {
+  constexpr int HT = HB / 2;               // heads per thread
+  extern __shared__ __align__(128) unsigned char sv_smem[];
+  double* gs = reinterpret_cast<double*>(sv_smem);                          // [STAGES][ROWS][SV_K]
+  double* rs = reinterpret_cast<double*>(sv_smem + SV_SMEM_G);             // [seg_len][HB]
+  const int rs_doubles = max(seg_len * HB, (SV_G - 1) * HB * SV_K);       // r, then the row-group partials
+  uint64_t* full = reinterpret_cast<uint64_t*>(rs + rs_doubles);
+  uint64_t* empty = full + SV_STAGES;
+  const int k0 = blockIdx.x * SV_K;
+  const int seg = blockIdx.y, h0 = blockIdx.z * HB;
   const int lbeg = seg * seg_len, lend = min(p, lbeg + seg_len);
-  const int t = threadIdx.x, tk = t / 8, tb = t % 8;      // rows k0+4tk.., heads b0+tb+8m
-  double acc[4][4] = {};
-  for (int l0 = lbeg; l0 < lend; l0 += SK_L) {
-    __syncthreads();
-    for (int e = t; e < SK_T * SK_L; e += 64) {
-      const int a = e / SK_L, l = e % SK_L;               // coalesced along l
-      Gs[l][a] = (k0 + a < p && l0 + l < lend) ? Ginv[(size_t)(k0 + a) * p + l0 + l] : 0.0;
-      Rs[l][a] = (b0 + a < BH && l0 + l < lend) ? r[(size_t)(b0 + a) * p + l0 + l] : 0.0;
+  const int nl = lend - lbeg;
+  const int nchunks = (nl + SV_ROWS - 1) / SV_ROWS;
+  const int kw = min(SV_K, ld - k0);       // columns of this tile inside the padded row (multiple of 32)
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  constexpr int CW = SV_CONS / 32;         // consumer warps
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < SV_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CW);
     }
-    __syncthreads();
-#pragma unroll 4
-    for (int l = 0; l < SK_L; ++l) {
-      double g[4], rv[4];
+    fence_mbar_init();
+  }
+  {   // stage r[h0 .. h0+HB)[lbeg .. lend) (L2-resident) with 8 independent loads in flight per thread
+    const int total = HB * seg_len;
+    for (int e0 = 0; e0 < total; e0 += 8 * (int)blockDim.x) {
+      double v[8];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        g[i] = Gs[l][tk * 4 + i];
-        rv[i] = Rs[l][tb + 8 * i];
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * (int)blockDim.x + (int)threadIdx.x;
+        const int h = e / seg_len, l = e % seg_len;   // coalesced along l
+        v[u] = (e < total && h0 + h < BH && l < nl) ? __ldg(r + (size_t)(h0 + h) * p + lbeg + l) : 0.0;
       }
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int m = 0; m < 4; ++m) acc[i][m] = fma(g[i], rv[m], acc[i][m]);
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * (int)blockDim.x + (int)threadIdx.x;
+        if (e < total) rs[(e % seg_len) * HB + e / seg_len] = v[u];
+      }
     }
   }
+  __syncthreads();
+  const int kq = threadIdx.x % 32;         // column quad: columns 4 kq .. 4 kq + 3
+  const int hh = (threadIdx.x / 32) % 2;   // head half: heads hh HT .. + HT
+  const int g = (threadIdx.x / 64);        // row group (consumers: 0..3)
+  double acc[4][HT];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int c = 0; c < 4; ++c)
 #pragma unroll
-    for (int m = 0; m < 4; ++m) {
-      const int k = k0 + tk * 4 + i, b = b0 + tb + 8 * m;
-      if (k < p && b < BH) part[((size_t)seg * BH + b) * p + k] = acc[i][m];
+    for (int h = 0; h < HT; ++h) acc[c][h] = 0.0;
+  if (warp == CW) {
+    // ---------------------------------------------------------------- producer: lane = row of the stage
+    for (int c = 0; c < nchunks; ++c) {
+      const int s = c % SV_STAGES;
+      if (c >= SV_STAGES) mbar_wait(&empty[s], ((c / SV_STAGES) - 1) & 1);
+      const int rows = min(SV_ROWS, nl - c * SV_ROWS);
+      (void)rows;
+      if (lane == 0) {
+        // one 32 x 128 box (32 KB); rows / columns outside the {ld, p} map are zero-filled by the TMA
+        // engine and still count towards the transaction bytes.  Rows past this segment's end belong to
+        // the next segment; the consumers skip them.
+        mbar_arrive_expect_tx(&full[s], (uint32_t)(SV_ROWS * SV_K * 8));
+        tma_load_2d(gs + (size_t)s * SV_ROWS * SV_K, &tm, &full[s], k0, lbeg + c * SV_ROWS);
+      }
     }
+  } else {
+    // ---------------------------------------------------------------- consumers
+    for (int c = 0; c < nchunks; ++c) {
+      const int s = c % SV_STAGES;
+      mbar_wait(&full[s], (c / SV_STAGES) & 1);
+      const int rows = min(SV_ROWS, nl - c * SV_ROWS);
+      const double* gr = gs + (size_t)s * SV_ROWS * SV_K + 4 * kq;
+      const double* rr = rs + (size_t)c * SV_ROWS * HB + hh * HT;
+      if (4 * kq < kw) {
+#pragma unroll 2
+        for (int i = g; i < rows; i += SV_G) {
+          const double2 ga = *reinterpret_cast<const double2*>(gr + i * SV_K);
+          const double2 gb = *reinterpret_cast<const double2*>(gr + i * SV_K + 2);
+          const double gv[4] = {ga.x, ga.y, gb.x, gb.y};
+          const double2* r2 = reinterpret_cast<const double2*>(rr + i * HB);
+#pragma unroll
+          for (int h = 0; h < HT / 2; ++h) {
+            const double2 x = r2[h];
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) {
+              acc[cc][2 * h] = fma(gv[cc], x.x, acc[cc][2 * h]);
+              acc[cc][2 * h + 1] = fma(gv[cc], x.y, acc[cc][2 * h + 1]);
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+  }
+  __syncthreads();   // rs is dead: reuse it for the row-group partials [g-1][head][k]
+  double* red = rs;
+  if (warp < CW && g > 0) {
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc)
+#pragma unroll
+      for (int h = 0; h < HT; ++h) red[((g - 1) * HB + hh * HT + h) * SV_K + 4 * kq + cc] = acc[cc][h];
+  }
+  __syncthreads();
+  if (warp < CW && g == 0) {
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+      const int k = k0 + 4 * kq + cc;
+      if (k >= p) continue;
+#pragma unroll
+      for (int h = 0; h < HT; ++h) {
+        double v = acc[cc][h];
+        for (int gg = 1; gg < SV_G; ++gg) v += red[((gg - 1) * HB + hh * HT + h) * SV_K + 4 * kq + cc];
+        if (h0 + hh * HT + h < BH) part[((size_t)seg * BH + h0 + hh * HT + h) * p + k] = v;
+      }
+    }
+  }
 }
 
 __global__ void solve_reduce_kernel(const double* __restrict__ part, double* __restrict__ X, int p, int BH, int nseg) {
@@ -119,10 +262,11 @@ __global__ void solve_reduce_kernel(const double* __restrict__ part, double* __r
 __global__ void __launch_bounds__(256) nae_partial_kernel(const float* __restrict__ U, const double* __restrict__ X,
                                                            const int* __restrict__ frame_ab,
                                                            const int* __restrict__ row_frames,
-                                                           double* __restrict__ out, int n, int p, int tiles) {
+                                                           double* __restrict__ out, int n, int p, int tiles,
+                                                           int rows) {
   const size_t bh = blockIdx.y;
   const int tile = blockIdx.x;
-  const int i0 = tile * kProjRows, i1 = min(i0 + kProjRows, n);
+  const int i0 = tile * rows, i1 = min(i0 + rows, n);
   const float* Uh = U + bh * (size_t)n * n;
   const double* x = X + bh * (size_t)p;
   double res = 0.0, nrm = 0.0;
@@ -214,17 +358,26 @@ mod_status fit_from_map(mod_plan P, const float* U, double* X, void* ws, cudaStr
   const int BH = P->L.batch * P->L.heads, n = P->n, p = P->p, tiles = P->proj_tiles;
   double* part = reinterpret_cast<double*>(static_cast<char*>(ws) + P->ws_part);
   double* r = reinterpret_cast<double*>(static_cast<char*>(ws) + P->ws_r);
-  project_kernel<<<dim3(tiles, BH), 256, 0, s>>>(U, part, P->d_frame_ab, n, P->F, p, tiles);
+  const int smem = (P->proj_rows * n + 8) * (int)sizeof(float);
+  MOD_CUDA(cudaFuncSetAttribute(project_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  project_kernel<<<dim3(tiles, BH), 256, smem, s>>>(U, part, P->d_frame_ab, n, P->F, p, tiles, P->proj_rows);
   MOD_LAUNCH_CHECK();
   const size_t tot = (size_t)BH * p;
   reduce_rhs_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(part, r, p, tiles, BH);
   MOD_LAUNCH_CHECK();
-  const int seg_len = ((p + SK_SEG - 1) / SK_SEG + SK_L - 1) / SK_L * SK_L;
   double* spart = reinterpret_cast<double*>(static_cast<char*>(ws) + P->ws_solve);
-  solve_partial_kernel<<<dim3((p + SK_T - 1) / SK_T, (BH + SK_T - 1) / SK_T, SK_SEG), 64, 0, s>>>(P->d_ginv, r, spart, p,
-                                                                                             BH, seg_len);
+  const dim3 sg((p + SV_K - 1) / SV_K, P->solve_segs, BH <= 8 ? 1 : (BH + 23) / 24);
+  const int hb = BH <= 8 ? 8 : 24;
+  const int ssmem = SV_SMEM_G + std::max(P->solve_seg_len * hb, (SV_G - 1) * hb * SV_K) * 8 + 2 * SV_STAGES * 8;
+  if (BH <= 8) {
+    MOD_CUDA(cudaFuncSetAttribute(solve_stream_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, ssmem));
+    solve_stream_kernel<8><<<sg, SV_THREADS, ssmem, s>>>(P->tm_ginv, P->ginv_ld, r, spart, p, BH, P->solve_seg_len);
+  } else {
+    MOD_CUDA(cudaFuncSetAttribute(solve_stream_kernel<24>, cudaFuncAttributeMaxDynamicSharedMemorySize, ssmem));
+    solve_stream_kernel<24><<<sg, SV_THREADS, ssmem, s>>>(P->tm_ginv, P->ginv_ld, r, spart, p, BH, P->solve_seg_len);
+  }
   MOD_LAUNCH_CHECK();
-  solve_reduce_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(spart, X, p, BH, SK_SEG);
+  solve_reduce_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(spart, X, p, BH, P->solve_segs);
   MOD_LAUNCH_CHECK();
   return MOD_OK;
 }
@@ -243,7 +396,7 @@ extern "C" mod_status mod_fit_mixture(mod_plan P, const float* stats, double* x,
     const int BH = P->L.batch * P->L.heads, tiles = P->proj_tiles;
     double* part = reinterpret_cast<double*>(static_cast<char*>(ws) + P->ws_nae);
     nae_partial_kernel<<<dim3(tiles, BH), 256, 0, s>>>(stats, x, P->d_frame_ab, P->d_row_frames, part, P->n, P->p,
-                                                       tiles);
+                                                       tiles, P->proj_rows);
     MOD_LAUNCH_CHECK();
     nae_final_kernel<<<(BH + 127) / 128, 128, 0, s>>>(part, nae, tiles, BH);
     MOD_LAUNCH_CHECK();

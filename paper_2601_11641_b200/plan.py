@@ -89,6 +89,9 @@ class Plan:
         mp, nd = C.c_double(), C.c_int32()
         check(lib.mod_plan_diagnostics(h, C.byref(mp), C.byref(nd)))
         self.min_pivot, self.null_dim = mp.value, nd.value
+        # App. B P:1251-1270 solver chain step that produced the Gram inverse, and the plan build time
+        self.solver = ("cholesky", "lu", "pinv")[lib.mod_plan_solver(h)]
+        self.create_ms = lib.mod_plan_create_ms(h)
         self.ws_bytes = lib.mod_plan_workspace_bytes(h)
         self._ws = {}        # one workspace per CUDA stream (moddit.h: concurrent calls need their own)
         # softmax scale s: 1/sqrt(head_dim) unless given

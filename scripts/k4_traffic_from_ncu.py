@@ -15,7 +15,7 @@ raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_outpu
 rows = list(csv.reader(raw.splitlines()))
 h, u, v = rows[0], rows[1], rows[2]
 val = lambda m: float(v[h.index(m)].replace(",", "")) * UNIT[u[h.index(m)]]
-name = re.sub(r"^void\s+", "", v[h.index("Kernel Name")].split("(")[0]).replace("<unnamed>::", "").replace(" ", "")
+name = re.sub(r"^void\s+", "", v[h.index("Kernel Name")].split("(")[0]).replace("<unnamed>::", "").replace("(int)", "").replace(" ", "")
 path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "k4_traffic.json")
 d = json.load(open(path)) if os.path.exists(path) else {}
 d = {k: x for k, x in d.items() if isinstance(x, dict)}

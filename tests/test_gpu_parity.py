@@ -548,3 +548,39 @@ def test_exact_sparsity_hunyuan_sampled_rows(M):
         d = np.abs((-Un[i][sel]) - row[sel])
         # K4's lse (<= 5e-3) and fp32 dot products move the few probabilities that sit at eta
         assert d.max() <= 0.02 and d.mean() <= 2e-3, (i, d.max(), d.mean())
+
+
+# ------------------------------------------------------------------------------------------ App. B solver chain
+# Layouts whose frame squares create linear dependencies among the bases that the plan's analytic
+# null-space list does not know (sub-block frames at the grid corner): the deflated Gram keeps a pivot of
+# order lambda, the Cholesky step is rejected and the chain of App. B must end in the
+# pseudo-inverse step.  X must still match the oracle's literal Tikhonov solve off null(M).
+DEGENERATE = [syn.Workload("degen-2x48", 1, 2, 64, 0, 2, 1, 48, 64),        # frames [0,0], [0,1]
+              syn.Workload("degen-prefix", 1, 2, 64, 10, 4, 2, 20, 64),     # nullity 3, analytic 1
+              syn.Workload("degen-6x3x14", 1, 2, 64, 0, 6, 3, 14, 64)]
+
+
+@pytest.mark.parametrize("w", DEGENERATE, ids=lambda w: w.name)
+def test_plan_solver_chain_degenerate_layout(M, w):
+    L = olayout(w)
+    Mx = O.design_matrix(L)
+    nullity = L.p - np.linalg.matrix_rank(Mx)
+    P = plan_for(M, w)
+    assert P.solver == "pinv", (P.solver, P.min_pivot, P.null_dim)
+    assert P.null_dim == nullity
+    assert P.min_pivot > 1e-4           # every retained direction is well conditioned after the chain
+    U = syn.random_stats(w.batch, w.heads, L.n, seed=17, device="cuda")
+    X = P.fit_mixture(U)
+    torch.cuda.synchronize()
+    xr = O.fit_mixture(U.double().cpu().numpy(), L)
+    _check_x(X.cpu().numpy(), xr, L, np.linalg.cond(O.gram_closed_form(L)))
+    # the pseudo-inverse solution is the minimum-norm least-squares fit: orthogonal to null(M)
+    V = _null_basis(L)
+    xg = X.cpu().numpy().reshape(-1, L.p)
+    assert np.abs(xg @ V).max() <= 1e-9 * np.abs(xg).max()
+
+
+@pytest.mark.parametrize("w", [TINY, SMALL_PREFIX, syn.HUNYUAN], ids=lambda w: w.name)
+def test_plan_solver_chain_video_layouts_stay_cholesky(M, w):
+    P = plan_for(M, w)
+    assert P.solver == "cholesky" and P.min_pivot > 1e-4 and P.create_ms > 0
