@@ -75,8 +75,7 @@ typedef enum {
 typedef enum {
   MOD_ATTN_DEFAULT = 0,     /* one 8-warp softmax group over column halves, NS S buffers ahead of it */
   MOD_ATTN_SPLITKV = 1,     /* two 4-warp softmax groups splitting the index list (round-1 kernel) */
-  MOD_ATTN_PAIR = 2,        /* two query blocks per CTA walking their merged index list (f4) */
-  MOD_ATTN_PAIR2 = 3        /* CTA pair, cta_group::2 M = 256 MMAs over two rows' lists (f4; D = 128) */
+  MOD_ATTN_PAIR = 2         /* two query blocks per CTA walking their merged index list (f4) */
 } mod_attn_kernel;
 
 typedef struct {

@@ -1067,339 +1067,6 @@ __global__ void __launch_bounds__(320, 1)
 }
 
 
-// ================================================================================================
-// ================================================================================================
-// CTA-pair K4 (MOD_ATTN_KERNEL=pair2; D = 128, 128-token blocks): a cluster of 2 CTAs on the two SMs
-// of a TPC owns query blocks 2p (CTA 0, the leader) and 2p+1 (CTA 1).  The leader's single thread
-// walks the UNION of the two index lists and issues M = 256 tcgen05.mma.cta_group::2 MMAs: each CTA
-// holds its 128 Q rows, half of each K tile's keys and half of each V tile's D columns (32 KB of K/V
-// per block per SM instead of 64 KB), and half the MMA instructions per FLOP are issued.  A union
-// entry that is not in a CTA's own list gets P = 0 without exponentials (the union costs tensor time,
-// not softmax time).  Split-KV softmax groups inside each CTA as in attn_fwd_kernel.
-template <int D>
-struct Pair2Cfg {
-  static constexpr int BN = 128, BM = 128, NATOM = D / 64;
-  static constexpr int Q_BOX = BM * 128, Q_BYTES = Q_BOX * NATOM;   // own 128 rows, all D
-  static constexpr int K_BOX = 64 * 128, K_BYTES = K_BOX * NATOM;   // 64 keys (this CTA's half), all D
-  static constexpr int V_BYTES = BN * 128;                          // 128 keys, 64 D columns (this CTA's half)
-  static constexpr int OFF_Q = 0, OFF_K = Q_BYTES, OFF_V = OFF_K + 2 * K_BYTES, OFF_BAR = OFF_V + 2 * V_BYTES;
-  static constexpr int NUM_BARS = 11;   // q_full, k_full[2], v_full[2], s_full[2], p_full[2], o_done[2]
-  static constexpr int OFF_RED = OFF_BAR + NUM_BARS * 8 + 16;
-  static constexpr int OFF_BITS = OFF_RED + 2 * 2 * 128 * 4;         // then: bitmaps, prefix counts, union
-  static constexpr int TMEM_O = 2 * BN;
-  static constexpr uint32_t IDESC_S = idesc_bf16_f32(256, BN, false, false);
-  static constexpr uint32_t IDESC_O = idesc_bf16_f32(256, D, false, true);
-};
-
-template <int D>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
-    attn_pair2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k64,
-                      const __grid_constant__ CUtensorMap tm_v, const int* __restrict__ row_ptr,
-                      const int* __restrict__ col_idx, __nv_bfloat16* __restrict__ out, float* __restrict__ lse,
-                      int N, int n, float scale_log2) {
-  using C = Pair2Cfg<D>;
-  constexpr int BN = C::BN;
-  extern __shared__ __align__(1024) unsigned char smem[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
-  uint64_t* q_full = bars;
-  uint64_t* k_full = bars + 1;
-  uint64_t* v_full = bars + 3;
-  uint64_t* s_full = bars + 5;
-  uint64_t* p_full = bars + 7;
-  uint64_t* o_done = bars + 9;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
-  const int W = (n + 31) / 32;   // bitmap words
-  uint32_t* bits = reinterpret_cast<uint32_t*>(smem + C::OFF_BITS);   // [2][W]: lists of rows 2p, 2p+1
-  int* prefix = reinterpret_cast<int*>(bits + 2 * W);                  // [W + 1]
-  uint16_t* ucol = reinterpret_cast<uint16_t*>(prefix + W + 1);        // union, ascending
-
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const uint32_t rank = cluster_ctarank();
-  const bool leader = rank == 0;
-  const int npair = (n + 1) >> 1;
-  const int cl = blockIdx.x >> 1;
-  const int bh = cl / npair, q0 = 2 * (cl % npair), qi = q0 + (int)rank;
-  // --- union of the two lists as bitmaps + prefix popcounts (identical in both CTAs)
-  for (int w = threadIdx.x; w < 2 * W; w += blockDim.x) bits[w] = 0u;
-  __syncthreads();
-  const int* rp = row_ptr + (size_t)bh * (n + 1);
-#pragma unroll
-  for (int x = 0; x < 2; ++x) {
-    const int row = q0 + x;
-    if (row < n) {
-      const int beg = rp[row], len = rp[row + 1] - beg;
-      const int* cols = col_idx + (size_t)bh * n * n + beg;
-      for (int e = threadIdx.x; e < len; e += blockDim.x) atomicOr(&bits[x * W + cols[e] / 32], 1u << (cols[e] % 32));
-    }
-  }
-  __syncthreads();
-  if (warp == 0) {
-    int run = 0;
-    for (int w0 = 0; w0 < W; w0 += 32) {
-      const int w = w0 + lane;
-      const int c = w < W ? __popc(bits[w] | bits[W + w]) : 0;
-      int incl = c;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      if (w < W) prefix[w] = run + incl - c;
-      run += __shfl_sync(0xffffffffu, incl, 31);
-    }
-    if (lane == 0) prefix[W] = run;
-  }
-  __syncthreads();
-  const int L = prefix[W];
-  for (int w = threadIdx.x; w < W; w += blockDim.x) {
-    uint32_t u = bits[w] | bits[W + w];
-    int pos = prefix[w];
-    while (u) {
-      const int b = __ffs(u) - 1;
-      ucol[pos++] = (uint16_t)(w * 32 + b);
-      u &= u - 1;
-    }
-  }
-  if (threadIdx.x == 0) {
-    mbar_init(q_full, 1);
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&k_full[s], 1);
-      mbar_init(&v_full[s], 1);
-      mbar_init(&s_full[s], 1);
-      mbar_init(&p_full[s], 8);     // one elected lane per softmax warp, 4 warps in each CTA
-      mbar_init(&o_done[s], 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 1) tmem_alloc_pair<512>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync_all();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer (both CTAs)
-    if (lane == 0 && L > 0) {
-      const uint64_t pol_q = policy_evict_first(), pol_kv = policy_evict_last();
-      auto lbar = [&](uint64_t* b) { return mapa_shared(smem_u32(b), 0); };   // leader's barrier
-      if (leader) mbar_arrive_expect_tx(q_full, 2 * C::Q_BYTES);
-#pragma unroll
-      for (int a = 0; a < C::NATOM; ++a)
-        tma_load_3d_pair(smem + C::OFF_Q + a * C::Q_BOX, &tm_q, lbar(q_full), a * 64, qi * BN, bh, pol_q);
-      auto load_k = [&](int u) {
-        const int s = u & 1;
-        if (u >= 2) mbar_wait(&s_full[s], ((u - 2) >> 1) & 1);   // S_{u-2} (multicast commit) read slot s
-        if (leader) mbar_arrive_expect_tx(&k_full[s], 2 * C::K_BYTES);
-        const int row = (int)ucol[u] * BN + (int)rank * 64;
-#pragma unroll
-        for (int a = 0; a < C::NATOM; ++a)
-          tma_load_3d_pair(smem + C::OFF_K + s * C::K_BYTES + a * C::K_BOX, &tm_k64, lbar(&k_full[s]), a * 64, row,
-                           bh, pol_kv);
-      };
-      auto load_v = [&](int u) {
-        const int s = u & 1;
-        if (u >= 2) mbar_wait(&o_done[s], ((u - 2) >> 1) & 1);   // PV_{u-2} read slot s
-        if (leader) mbar_arrive_expect_tx(&v_full[s], 2 * C::V_BYTES);
-        tma_load_3d_pair(smem + C::OFF_V + s * C::V_BYTES, &tm_v, lbar(&v_full[s]), (int)rank * 64,
-                         (int)ucol[u] * BN, bh, pol_kv);
-      };
-      load_k(0);
-      for (int u = 0; u < L; ++u) {
-        if (u + 1 < L) load_k(u + 1);
-        load_v(u);
-      }
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer (leader CTA only)
-    if (leader && lane == 0 && L > 0) {
-      mbar_wait_cluster(q_full, 0);
-      tc_fence_after();
-      const uint64_t a_base = smem_desc_sw128(smem_u32(smem + C::OFF_Q), 16, 1024);
-      auto issue_s = [&](int u, int b) {
-        mbar_wait_cluster(&k_full[b], (u >> 1) & 1);
-        const uint64_t b_base = smem_desc_sw128(smem_u32(smem + C::OFF_K + b * C::K_BYTES), 16, 1024);
-        const uint32_t d_s = tmem + b * BN;
-        static_for<D / 16>([&](auto kc) {
-          constexpr int kk = decltype(kc)::value;
-          mma2_ss_off<((kk / 4) * C::Q_BOX + (kk % 4) * 32) / 16, ((kk / 4) * C::K_BOX + (kk % 4) * 32) / 16>(
-              d_s, a_base, b_base, C::IDESC_S, kk > 0 ? 1u : 0u);
-        });
-        mma2_commit_both(&s_full[b]);
-      };
-      auto pv_then_s = [&](int u, int b) {
-        mbar_wait_cluster(&v_full[b], (u >> 1) & 1);
-        mbar_wait_cluster(&p_full[b], (u >> 1) & 1);
-        tc_fence_after();
-        const uint64_t v_base = smem_desc_sw128(smem_u32(smem + C::OFF_V + b * C::V_BYTES), C::V_BYTES, 1024);
-        const uint32_t acc0 = u > 1 ? 1u : 0u;
-        static_for<BN / 16>([&](auto kc) {
-          constexpr int kk = decltype(kc)::value;
-          mma2_ts_off<kk * 8, kk * 2048 / 16>(tmem + C::TMEM_O + b * D, tmem + b * BN, v_base, C::IDESC_O,
-                                              kk > 0 ? 1u : acc0);
-        });
-        mma2_commit_both(&o_done[b]);
-        if (u + 2 < L) issue_s(u + 2, b);
-      };
-      issue_s(0, 0);
-      if (L > 1) issue_s(1, 1);
-      for (int u = 0; u < L; u += 2) {
-        pv_then_s(u, 0);
-        if (u + 1 < L) pv_then_s(u + 1, 1);
-      }
-    }
-  } else {
-    // ------------------------------------------------------------ softmax / epilogue (2 groups x 4 warps)
-    const int g = (warp - 2) >> 2;
-    const int quarter = warp & 3;
-    const int row = quarter * 32 + lane;
-    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-    const uint32_t t_s = tmem + lane_off + (g ? BN : 0);
-    const uint32_t t_og = tmem + lane_off + C::TMEM_O + g * D;
-    const uint32_t p_full_leader = mapa_shared(smem_u32(&p_full[g]), 0);
-    const uint32_t* own = bits + rank * W;
-    float m_run = -INFINITY, l_run = 0.f;
-    int it = 0;
-    for (int u = g; u < L; u += 2, ++it) {
-      mbar_wait(&s_full[g], it & 1);
-      tc_fence_after();
-      const int col = ucol[u];
-      const bool member = (own[col >> 5] >> (col & 31)) & 1u;
-      uint32_t pk[BN / 2];
-      float alpha = 1.0f;
-      bool rescale = false;
-      if (member) {
-        uint32_t sr[BN];
-#pragma unroll
-        for (int c = 0; c < BN / 32; ++c) tmem_ld32(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
-        tmem_ld_wait();
-        float* s = reinterpret_cast<float*>(sr);
-        const int kv_valid = N - col * BN;
-        if (kv_valid < BN) {
-#pragma unroll
-          for (int c = 0; c < BN; ++c)
-            if (c >= kv_valid) s[c] = -INFINITY;
-        }
-        float mxv[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) mxv[e] = s[e];
-#pragma unroll
-        for (int c = 8; c < BN; c += 8)
-#pragma unroll
-          for (int e = 0; e < 8; ++e) mxv[e] = fmaxf(mxv[e], s[c + e]);
-        const float mx = fmaxf(fmaxf(fmaxf(mxv[0], mxv[1]), fmaxf(mxv[2], mxv[3])),
-                               fmaxf(fmaxf(mxv[4], mxv[5]), fmaxf(mxv[6], mxv[7])));
-        const float m_new = fmaxf(m_run, mx * scale_log2);
-        rescale = (m_new - m_run) > 8.0f;
-        const float m_use = rescale ? m_new : m_run;
-        alpha = rescale ? ex2(m_run - m_new) : 1.0f;
-        const float2 sc2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-m_use, -m_use);
-        float2 acc2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#pragma unroll
-        for (int c = 0; c < BN; c += 2) {
-          const float2 x = ffma2(make_float2(s[c], s[c + 1]), sc2, nm2);
-          float2 p;
-          if (((c / 2) & 7) < kEmuPairsPer8) {
-            p = ex2_poly2(x);
-          } else {
-            p.x = ex2(x.x);
-            p.y = ex2(x.y);
-          }
-          acc2[(c / 2) & 1] = fadd2(acc2[(c / 2) & 1], p);
-          pk[c / 2] = pack_bf16(p.x, p.y);
-        }
-        l_run = fmaf(l_run, alpha, (acc2[0].x + acc2[0].y) + (acc2[1].x + acc2[1].y));
-        m_run = m_use;
-      } else {
-#pragma unroll
-        for (int c = 0; c < BN / 2; ++c) pk[c] = 0u;   // not in this row's list: P = 0, no exponentials
-      }
-#pragma unroll
-      for (int c = 0; c < BN / 64; ++c) tmem_st32(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[c * 32]));
-      if (it >= 1) {
-        mbar_wait(&o_done[g], (it - 1) & 1);
-        tc_fence_after();
-        if (__any_sync(0xffffffffu, rescale)) {
-#pragma unroll
-          for (int c = 0; c < D / 32; ++c) {
-            uint32_t o[32];
-            tmem_ld32(t_og + c * 32, o);
-            tmem_ld_wait();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-            tmem_st32(t_og + c * 32, o);
-          }
-        }
-      }
-      tmem_st_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(p_full_leader);   // one (remote) arrival per warp
-    }
-    // epilogue: merge the two split-KV partials of this CTA's row block
-    auto red = reinterpret_cast<float(*)[2][128]>(smem + C::OFF_RED);
-    red[g][0][row] = m_run;
-    red[g][1][row] = l_run;
-    named_bar_sync(1, 256);
-    const int n0 = (L + 1) / 2, n1 = L / 2;
-    const float m0 = red[0][0][row], l0 = red[0][1][row], m1 = red[1][0][row], l1 = red[1][1][row];
-    if (qi < n) {
-      const int q_row0 = qi * BN;
-      const bool valid = row < min(BN, N - q_row0);
-      const size_t grow = (size_t)bh * N + q_row0 + row;
-      const float l_tot_probe = l0 + l1;
-      if (L > 0) {
-        mbar_wait(&o_done[0], (n0 - 1) & 1);
-        if (n1 > 0) mbar_wait(&o_done[1], (n1 - 1) & 1);
-        tc_fence_after();
-      }
-      if (L > 0 && l_tot_probe > 0.f) {
-        const float m = fmaxf(m0, m1);
-        const float f0 = l0 > 0.f ? ex2(m0 - m) : 0.f;
-        const float f1 = l1 > 0.f ? ex2(m1 - m) : 0.f;
-        const float l = l0 * f0 + l1 * f1;
-        const float a0 = f0 / l, a1 = f1 / l;
-        const uint32_t t_o0 = tmem + lane_off + C::TMEM_O + g * (D / 2);
-#pragma unroll
-        for (int c = 0; c < D / 64; ++c) {
-          uint32_t o0[32], o1[32];
-          tmem_ld32(t_o0 + c * 32, o0);
-          tmem_ld32(t_o0 + D + c * 32, o1);
-          tmem_ld_wait();
-          uint32_t pkd[16];
-#pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            float x0 = __uint_as_float(o0[2 * e]) * a0, x1 = __uint_as_float(o0[2 * e + 1]) * a0;
-            if (n1 > 0) {
-              x0 = fmaf(__uint_as_float(o1[2 * e]), a1, x0);
-              x1 = fmaf(__uint_as_float(o1[2 * e + 1]), a1, x1);
-            }
-            pkd[e] = pack_bf16(x0, x1);
-          }
-          if (valid) {
-            int4* dst = reinterpret_cast<int4*>(out + grow * D + g * (D / 2) + c * 32);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) dst[e] = make_int4(pkd[4 * e], pkd[4 * e + 1], pkd[4 * e + 2], pkd[4 * e + 3]);
-          }
-        }
-        if (valid && lse && g == 0) lse[grow] = (m + __log2f(l)) * 0.69314718055994531f;
-      } else if (valid) {   // no listed block (the partner's list may not be empty): O = 0, lse = -inf
-        int4* dst = reinterpret_cast<int4*>(out + grow * D + g * (D / 2));
-#pragma unroll
-        for (int e = 0; e < D / 16; ++e) dst[e] = make_int4(0, 0, 0, 0);
-        if (lse && g == 0) lse[grow] = -INFINITY;
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync_all();
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc_pair<512>(tmem);
-  }
-}
-
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -1480,31 +1147,8 @@ mod_status launch_pair(mod_plan P, const void* q, const void* k, const void* v, 
   return MOD_OK;
 }
 
-mod_status launch_pair2(mod_plan P, const void* q, const void* k, const void* v, const int* row_ptr,
-                        const int* col_idx, void* o, float* lse, cudaStream_t s) {
-  constexpr int D = 128;
-  using C = Pair2Cfg<D>;
-  const int BH = P->L.batch * P->L.heads;
-  CUtensorMap tq, tk, tv;
-  mod_status st;
-  if ((st = make_map(&tq, q, BH, P->N, D, 128)) != MOD_OK) return st;
-  if ((st = make_map(&tk, k, BH, P->N, D, 64)) != MOD_OK) return st;    // half a key block
-  if ((st = make_map(&tv, v, BH, P->N, D, 128)) != MOD_OK) return st;   // one 64-column box of 128 keys
-  const int W = (P->n + 31) / 32;
-  const int smem = C::OFF_BITS + 2 * W * 4 + (W + 1) * 4 + 2 * (2 * P->n) + 16;
-  MOD_REQUIRE(smem <= 232448, MOD_ERR_INPUT, "pair2 kernel: n=%d too large", P->n);
-  auto kern = attn_pair2_kernel<D>;
-  MOD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  const float scale_log2 = P->scale * 1.4426950408889634f;
-  const int npair = (P->n + 1) / 2;
-  kern<<<BH * npair * 2, 320, smem, s>>>(tq, tk, tv, row_ptr, col_idx, (__nv_bfloat16*)o, lse, P->N, P->n,
-                                         scale_log2);
-  MOD_LAUNCH_CHECK();
-  return MOD_OK;
-}
-
 // The schedule a plan runs: its config's attn_kernel where that variant supports the layout (pair:
-// 128-token blocks, both lists in shared memory; pair2: additionally D = 128), else the default.
+// 128-token blocks, both lists in shared memory), else the default.
 int effective_kernel(mod_plan P) {
   const int want = P->cfg.attn_kernel;
   if (want == MOD_ATTN_PAIR) {
@@ -1512,7 +1156,6 @@ int effective_kernel(mod_plan P) {
     if (P->L.block == 128 && P->n <= cap && P->n <= 65535) return MOD_ATTN_PAIR;
     return MOD_ATTN_DEFAULT;
   }
-  if (want == MOD_ATTN_PAIR2) return (P->L.head_dim == 128 && P->L.block == 128) ? MOD_ATTN_PAIR2 : MOD_ATTN_DEFAULT;
   return want;
 }
 }  // namespace
@@ -1535,7 +1178,6 @@ extern "C" const char* mod_attn_kernel_name(mod_plan P) {
       return D == 128 ? (BN == 128 ? "attn_split_kernel<128,128>" : "attn_split_kernel<128,64>")
                       : (BN == 128 ? "attn_split_kernel<64,128>" : "attn_split_kernel<64,64>");
     case MOD_ATTN_PAIR: return D == 128 ? "attn_pair_kernel<128,128>" : "attn_pair_kernel<64,128>";
-    case MOD_ATTN_PAIR2: return "attn_pair2_kernel<128>";
     default:
       return D == 128 ? (BN == 128 ? "attn_fwd_kernel<128,128>" : "attn_fwd_kernel<128,64>")
                       : (BN == 128 ? "attn_fwd_kernel<64,128>" : "attn_fwd_kernel<64,64>");
@@ -1554,9 +1196,6 @@ extern "C" mod_status mod_block_sparse_attn_fwd(mod_plan P, const void* q, const
   cudaStream_t s = as_stream(stream);
   const int D = P->L.head_dim, BN = P->L.block;
   switch (effective_kernel(P)) {
-    case MOD_ATTN_PAIR2:
-      st = launch_pair2(P, q, k, v, row_ptr, col_idx, o, lse, s);
-      break;
     case MOD_ATTN_PAIR:
       st = D == 128 ? launch_pair<128>(P, q, k, v, row_ptr, col_idx, o, lse, s)
                     : launch_pair<64>(P, q, k, v, row_ptr, col_idx, o, lse, s);

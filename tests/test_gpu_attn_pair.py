@@ -1,7 +1,7 @@
 """K4 kernel schedules (Plan(attn_kernel=...), include/moddit.h mod_attn_kernel) against the fp64 oracle:
-the default one-softmax-group kernel, the round-1 split-KV kernel ("splitkv"), the paired-query-block
-kernel ("pair") and the CTA-pair kernel with M = 256 cta_group::2 MMAs over the union of
-two rows' lists ("pair2"; D = 128 only, other shapes run the default).
+the default kernel, the round-1 split-KV kernel ("splitkv") and the paired-query-block kernel ("pair";
+SURVEY §8(f) f4).  (The round-1 CTA-pair kernel with M = 256 cta_group::2 MMAs, "pair2", measured 25 %
+slower and was retired in round 2.)
 
 The pair kernel walks the merged index list of query blocks 2p and 2p+1 and shares each K/V tile
 between them, so its masks are chosen to exercise every shape of that merge: lists that coincide,
@@ -31,7 +31,7 @@ def M():
     return m
 
 
-KERNELS = ["default", "splitkv", "pair", "pair2"]
+KERNELS = ["default", "splitkv", "pair"]
 
 
 @pytest.fixture(params=KERNELS)
