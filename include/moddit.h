@@ -272,6 +272,13 @@ mod_status mod_ulysses_head_pack(const void* x_head, void* send, int32_t B, int3
                                  int32_t P, void* stream);
 mod_status mod_ulysses_head_unpack(const void* recv, void* x_seq, int32_t B, int32_t Ns, int32_t Hp, int32_t D,
                                    int32_t P, void* stream);
+/* Head-chunk variants for the overlapped (chunked) Ulysses exchange: seq_pack of heads [h0, h0+Hc) of an
+ * H-head x_seq [B,Ns,H,D] -> send [P,B,Ns,Hc/P,D] (Hc % P == 0); head_unpack of recv [P,B,Ns,Hp,D] into
+ * heads [h0, h0+P*Hp) of x_seq [B,Ns,H,D] (other heads untouched).  Same alignment / size rules. */
+mod_status mod_ulysses_seq_pack_heads(const void* x_seq, void* send, int32_t B, int32_t Ns, int32_t H, int32_t h0,
+                                      int32_t Hc, int32_t D, int32_t P, void* stream);
+mod_status mod_ulysses_head_unpack_heads(const void* recv, void* x_seq, int32_t B, int32_t Ns, int32_t Hp, int32_t D,
+                                         int32_t P, int32_t H, int32_t h0, void* stream);
 
 /* Number of kernels the last successful compute call on this thread launched (for bench.py). */
 int32_t mod_last_launch_count(void);

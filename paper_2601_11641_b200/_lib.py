@@ -81,6 +81,8 @@ SIGNATURES = {
     "mod_ulysses_seq_unpack": (I32, [P, P, I32, I32, I32, I32, I32, P]),
     "mod_ulysses_head_pack": (I32, [P, P, I32, I32, I32, I32, I32, P]),
     "mod_ulysses_head_unpack": (I32, [P, P, I32, I32, I32, I32, I32, P]),
+    "mod_ulysses_seq_pack_heads": (I32, [P, P, I32, I32, I32, I32, I32, I32, I32, P]),
+    "mod_ulysses_head_unpack_heads": (I32, [P, P, I32, I32, I32, I32, I32, I32, I32, P]),
 }
 
 

@@ -21,9 +21,13 @@ namespace {
 
 enum { SEQ_PACK = 0, SEQ_UNPACK = 1, HEAD_PACK = 2, HEAD_UNPACK = 3 };
 
-// 32-bit row arithmetic (the host checks rows < 2^31): 64-bit divisions would dominate the copy
+// 32-bit row arithmetic (the host checks rows < 2^31): 64-bit divisions would dominate the copy.
+// Ht / h0: the x_seq side may hold more heads than the exchanged group -- SEQ_PACK reads heads
+// [h0, h0 + P*Hp) of an [B, Ns, Ht] source and HEAD_UNPACK writes them into an [B, Ns, Ht] destination
+// (the head chunks of the overlapped Ulysses pipeline, parallel.py); Ht = P*Hp, h0 = 0 is the whole tensor.
 template <int MODE>
-__device__ __forceinline__ uint32_t src_row(uint32_t r, uint32_t B, uint32_t Ns, uint32_t Hp, uint32_t P) {
+__device__ __forceinline__ uint32_t src_row(uint32_t r, uint32_t B, uint32_t Ns, uint32_t Hp, uint32_t P,
+                                            uint32_t Ht, uint32_t h0) {
   if (MODE == SEQ_PACK || MODE == HEAD_PACK) {
     // destination [P, B, Ns, Hp]
     const uint32_t hp = r % Hp;
@@ -31,7 +35,7 @@ __device__ __forceinline__ uint32_t src_row(uint32_t r, uint32_t B, uint32_t Ns,
     const uint32_t s = t % Ns;
     t /= Ns;
     const uint32_t b = t % B, p = t / B;
-    if (MODE == SEQ_PACK) return (b * Ns + s) * (P * Hp) + p * Hp + hp;   // x_seq [B,Ns,H]
+    if (MODE == SEQ_PACK) return (b * Ns + s) * Ht + h0 + p * Hp + hp;    // x_seq [B,Ns,Ht]
     return (b * Hp + hp) * (P * Ns) + p * Ns + s;                         // x_head [B,Hp,N]
   } else if (MODE == SEQ_UNPACK) {
     // destination [B, Hp, P*Ns]
@@ -50,10 +54,18 @@ __device__ __forceinline__ uint32_t src_row(uint32_t r, uint32_t B, uint32_t Ns,
   }
 }
 
+// destination row index of enumerated row r: identity except for HEAD_UNPACK into a wider x_seq
+template <int MODE>
+__device__ __forceinline__ uint32_t dst_row(uint32_t r, uint32_t Hp, uint32_t P, uint32_t Ht, uint32_t h0) {
+  if (MODE != HEAD_UNPACK) return r;
+  const uint32_t H = P * Hp;
+  return (r / H) * Ht + h0 + r % H;
+}
+
 template <int MODE, int VPR>   // VPR = 16-byte vectors per row (D / 8)
 __global__ void __launch_bounds__(256) relayout_kernel(const int4* __restrict__ src, int4* __restrict__ dst,
                                                        uint32_t rows, uint32_t B, uint32_t Ns, uint32_t Hp,
-                                                       uint32_t P) {
+                                                       uint32_t P, uint32_t Ht, uint32_t h0) {
   // one row per VPR consecutive threads; 4 rows in flight per thread for memory-level parallelism
   constexpr int UNROLL = 4;
   const uint32_t c = threadIdx.x % VPR;
@@ -64,18 +76,23 @@ __global__ void __launch_bounds__(256) relayout_kernel(const int4* __restrict__ 
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) {
       const uint32_t r = r0 + u * rows_per_block;
-      if (r < rows) v[u] = __ldcs(src + (size_t)src_row<MODE>(r, B, Ns, Hp, P) * VPR + c);   // read once
+      if (r < rows) v[u] = __ldcs(src + (size_t)src_row<MODE>(r, B, Ns, Hp, P, Ht, h0) * VPR + c);   // read once
     }
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) {
       const uint32_t r = r0 + u * rows_per_block;
-      if (r < rows) __stcs(dst + (size_t)r * VPR + c, v[u]);
+      if (r < rows) __stcs(dst + (size_t)dst_row<MODE>(r, Hp, P, Ht, h0) * VPR + c, v[u]);
     }
   }
 }
 
 template <int MODE>
-mod_status launch(const void* src, void* dst, int B, int Ns, int Hp, int D, int P, void* stream) {
+mod_status launch(const void* src, void* dst, int B, int Ns, int Hp, int D, int P, void* stream, int Ht = -1,
+                  int h0 = 0) {
+  if (Ht < 0) Ht = P * Hp;
+  MOD_REQUIRE(h0 >= 0 && h0 + P * Hp <= Ht, MOD_ERR_INPUT, "ulysses relayout: heads [%d, %d) outside the %d heads",
+              h0, h0 + P * Hp, Ht);
+  MOD_REQUIRE((size_t)B * Ns * Ht < (1ull << 31), MOD_ERR_INPUT, "ulysses relayout: x_seq rows exceed 2^31");
   MOD_REQUIRE(src && dst, MOD_ERR_USAGE, "ulysses relayout: src and dst must be non-NULL");
   MOD_REQUIRE(B >= 1 && Ns >= 1 && Hp >= 1 && P >= 1, MOD_ERR_INPUT,
               "ulysses relayout: B=%d Ns=%d Hp=%d P=%d must all be >= 1", B, Ns, Hp, P);
@@ -94,9 +111,9 @@ mod_status launch(const void* src, void* dst, int B, int Ns, int Hp, int D, int 
   const int grid = (int)std::min<size_t>((rows + rows_per_cta - 1) / rows_per_cta, (size_t)sms * 8);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (D == 128)
-    relayout_kernel<MODE, 16><<<grid, 256, 0, s>>>((const int4*)src, (int4*)dst, (uint32_t)rows, B, Ns, Hp, P);
+    relayout_kernel<MODE, 16><<<grid, 256, 0, s>>>((const int4*)src, (int4*)dst, (uint32_t)rows, B, Ns, Hp, P, Ht, h0);
   else
-    relayout_kernel<MODE, 8><<<grid, 256, 0, s>>>((const int4*)src, (int4*)dst, (uint32_t)rows, B, Ns, Hp, P);
+    relayout_kernel<MODE, 8><<<grid, 256, 0, s>>>((const int4*)src, (int4*)dst, (uint32_t)rows, B, Ns, Hp, P, Ht, h0);
   MOD_LAUNCH_CHECK();
   mod_note_launches(1);
   return MOD_OK;
@@ -124,4 +141,18 @@ extern "C" mod_status mod_ulysses_head_pack(const void* x_head, void* send, int3
 extern "C" mod_status mod_ulysses_head_unpack(const void* recv, void* x_seq, int32_t B, int32_t Ns, int32_t Hp,
                                               int32_t D, int32_t P, void* stream) {
   return launch<HEAD_UNPACK>(recv, x_seq, B, Ns, Hp, D, P, stream);
+}
+
+// Head-chunk variants (the overlapped Ulysses pipeline): pack heads [h0, h0 + Hc) of an H-head x_seq, and
+// unpack into heads [h0, h0 + P*Hp) of an H-head x_seq.
+extern "C" mod_status mod_ulysses_seq_pack_heads(const void* x_seq, void* send, int32_t B, int32_t Ns, int32_t H,
+                                                 int32_t h0, int32_t Hc, int32_t D, int32_t P, void* stream) {
+  MOD_REQUIRE(P >= 1 && Hc >= 1 && Hc % P == 0, MOD_ERR_INPUT,
+              "mod_ulysses_seq_pack_heads: chunk of %d heads not divisible by P=%d", Hc, P);
+  return launch<SEQ_PACK>(x_seq, send, B, Ns, Hc / P, D, P, stream, H, h0);
+}
+
+extern "C" mod_status mod_ulysses_head_unpack_heads(const void* recv, void* x_seq, int32_t B, int32_t Ns, int32_t Hp,
+                                                    int32_t D, int32_t P, int32_t H, int32_t h0, void* stream) {
+  return launch<HEAD_UNPACK>(recv, x_seq, B, Ns, Hp, D, P, stream, H, h0);
 }

@@ -156,6 +156,27 @@ def family_s(w: Workload, seed: int = SEED_BASE, device="cpu", sigma: float = 0.
     return q, k, v
 
 
+def family_s_heads(w: Workload, heads, **kw):
+    """Family S for an arbitrary list of heads of ``w`` (e.g. a rank's LPT or Ulysses-chunk heads): the
+    heads are generated one at a time (``head_offset`` = h, ``total_heads`` = w.heads), so every head's
+    bytes equal those of the full tensor and at most one head is live beyond the output."""
+    outs = [family_s(w.with_heads(1), head_offset=int(h), total_heads=w.heads, **kw) for h in heads]
+    return tuple(torch.cat([o[i] for o in outs], dim=1) for i in range(3))
+
+
+def family_s_seq_shard(w: Workload, t0: int, t1: int, **kw):
+    """Tokens [t0, t1) of every head of Family S, in the sequence-sharded activation layout [B, t1-t0, H, D]
+    (the input of a Ulysses rank).  Generated head by head, so a rank never holds the full tensors."""
+    B, H, D = w.batch, w.heads, w.head_dim
+    dev = kw.get("device", "cpu")
+    outs = tuple(torch.empty((B, t1 - t0, H, D), dtype=torch.bfloat16, device=dev) for _ in range(3))
+    for h in range(H):
+        qkv = family_s(w.with_heads(1), head_offset=h, total_heads=H, **kw)
+        for dst, src in zip(outs, qkv):
+            dst[:, :, h] = src[:, 0, t0:t1]
+    return outs
+
+
 def random_stats(B: int, H: int, n: int, seed: int = SEED_BASE, device="cpu") -> torch.Tensor:
     """Row-stochastic fp32 block-statistic maps [B,H,n,n] (positive, rows sum to ~1)."""
     g = _gen(seed, device)

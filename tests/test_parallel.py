@@ -94,3 +94,24 @@ def test_relayout_reference_maps_p1():
     x = torch.randn(2, 5, 6, 8)
     assert torch.equal(seq_to_heads(x, relayout=TorchRelayout), x.permute(0, 2, 1, 3))
     assert torch.equal(heads_to_seq(x.permute(0, 2, 1, 3).contiguous(), relayout=TorchRelayout), x)
+
+
+def test_family_s_head_lists_and_sequence_shards_are_the_full_tensor_bytes():
+    """Per-rank generators (LPT head lists, Ulysses sequence shards) draw exactly the bytes of the full
+    tensors, so multi-rank runs and the single-GPU run see the same inputs."""
+    import synthetic as syn
+    w = syn.Workload("t", 1, 4, 64, 10, 2, 4, 4, 64)
+    q, k, v = syn.family_s(w, step=3)
+    q2, k2, v2 = syn.family_s_heads(w, [2, 0], step=3)
+    assert torch.equal(q2[:, 0], q[:, 2]) and torch.equal(k2[:, 1], k[:, 0]) and torch.equal(v2[:, 0], v[:, 2])
+    qs, ks, vs = syn.family_s_seq_shard(w, 5, 20, step=3)
+    for a, b in ((qs, q), (ks, k), (vs, v)):
+        assert torch.equal(a, b.permute(0, 2, 1, 3)[:, 5:20])
+
+
+def test_ulysses_chunk_heads_partition():
+    from paper_2601_11641_b200.parallel import ulysses_chunk_heads
+    for H, P, C in ((24, 2, 3), (24, 8, 3), (40, 4, 2), (4, 2, 2)):
+        owned = [ulysses_chunk_heads(H, P, C, r) for r in range(P)]
+        assert sorted(h for o in owned for h in o) == list(range(H))
+        assert all(len(o) == H // P for o in owned)
