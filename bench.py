@@ -159,7 +159,9 @@ def bisect_top_k(P, x_prev, x_curr, keep, target_sparsity: float, ws: int):
     def sparsity(K):
         rp, _ = P.predict_block_mask(x_prev, x_curr, M_WARMUP - 1, M_WARMUP, M_WARMUP + DT, keep, top_k=K)
         nnz = sum_over_ranks(float(rp[..., -1].sum().item()), ws)
-        return 1.0 - nnz / (P.BH * ws * n * n)
+        return 1.0 - nnz / (total_heads * n * n)
+
+    total_heads = sum_over_ranks(float(P.BH), ws)
 
     while lo < hi:
         mid = (lo + hi) // 2
@@ -199,19 +201,31 @@ def run_ours(args):
 
     ws, rank, local = dist_setup(args.gpus)
     w_full = syn.CONFIGS[args.config]
-    assert w_full.heads % ws == 0, f"heads {w_full.heads} not divisible by {ws} ranks"
-    Hl = w_full.heads // ws
-    h0 = rank * Hl
-    w = w_full.with_heads(Hl)
-    D, N, blk = w.head_dim, w.tokens, w.block
+    H = w_full.heads
+    from paper_2601_11641_b200.parallel import head_range, lpt_head_assignment, ulysses_chunk_heads
+    chunks_u = 0
+    if args.ulysses:
+        # config 5: activations arrive sequence-sharded [B, N/P, H, D]; UlyssesChunkPipeline exchanges head
+        # chunks (NCCL all_to_all_single over NVLink) overlapped with the hot path of the previous chunk
+        want = args.ulysses_chunks if args.ulysses_chunks > 0 else 3
+        chunks_u = max(c for c in range(1, want + 1) if H % (c * ws) == 0)
+        heads = ulysses_chunk_heads(H, ws, chunks_u, rank)
+    else:
+        heads = list(range(*head_range(H, ws, rank)))
+    D, N, blk = w_full.head_dim, w_full.tokens, w_full.block
     burst, sustained, hbm, peak_src = load_peaks()
 
     exact = args.stat == "exact"
-    P = Plan(w, top_k=1, tau_e=0.0, masked_renorm=not exact, attn_kernel=args.attn_kernel)
-    gen = dict(seed=syn.SEED_BASE, device="cuda", head_offset=h0, total_heads=w_full.heads)
+    plan_kw = dict(top_k=1, tau_e=0.0, masked_renorm=not exact, attn_kernel=args.attn_kernel)
     extra = {}
 
-    def warm_stat(qq, kk, vv):
+    def gen(step):   # this rank's heads of the step's Q, K, V (the bytes one GPU would draw for them)
+        if heads == list(range(heads[0], heads[0] + len(heads))):
+            return syn.family_s(w_full.with_heads(len(heads)), step=step, seed=syn.SEED_BASE, device="cuda",
+                                head_offset=heads[0], total_heads=H)
+        return syn.family_s_heads(w_full, heads, step=step, seed=syn.SEED_BASE, device="cuda")
+
+    def warm_stat(P, qq, kk, vv):
         """Statistic of a warm-up step: POOLED, or EXACT Eq. 2 from the dense attention's lse."""
         if not exact:
             return P.collect_block_stats(qq, kk)
@@ -226,29 +240,43 @@ def run_ours(args):
         extra["exact_dense_stat_ms"] = round(e_a.elapsed_time(e_b), 3)
         return U
 
-    # ---- warm-up phase of Alg. 1: statistics at t = m-1 and t = m, fits, keep decision
-    q1, k1, v1 = syn.family_s(w, step=M_WARMUP - 1, **gen)
-    W1 = warm_stat(q1, k1, v1)
-    del q1, k1, v1
-    seq = None
-    if args.ulysses:
-        # config 5: activations arrive sequence-sharded [B, N/P, H, D]; the step starts with the Ulysses
-        # all-to-all to head shards and ends with the inverse (NCCL all_to_all_single over NVLink)
-        from paper_2601_11641_b200.parallel import heads_to_seq, seq_to_heads
-        assert w_full.tokens % ws == 0, "tokens not divisible by world size"
-        full = syn.family_s(w_full, step=M_WARMUP, seed=syn.SEED_BASE, device="cuda")
-        Ns = w_full.tokens // ws
-        seq = [t.permute(0, 2, 1, 3)[:, rank * Ns:(rank + 1) * Ns].contiguous() for t in full]
-        del full
-        q, k, v = (seq_to_heads(t) for t in seq)
-    else:
-        q, k, v = syn.family_s(w, step=M_WARMUP, **gen)
-    W2 = warm_stat(q, k, v)
-    x_prev0, x_curr0 = P.fit_mixture(W1), P.fit_mixture(W2)
-    keep = P.keep_frames(x_prev0, x_curr0)
-    hist = W2.clone()                                  # A_hat^(t_p^(0)) = A^(m)
+    def warm_up():
+        """Warm-up phase of Alg. 1 for this rank's heads: statistics at t = m-1 and t = m,
+        fits, keep decision, history (untimed setup)."""
+        P_ = Plan(w_full.with_heads(len(heads)), **plan_kw)
+        q1, k1, v1 = gen(M_WARMUP - 1)
+        W1_ = warm_stat(P_, q1, k1, v1)
+        del q1, k1, v1
+        q_, k_, v_ = gen(M_WARMUP)
+        W2_ = warm_stat(P_, q_, k_, v_)
+        xp, xc = P_.fit_mixture(W1_), P_.fit_mixture(W2_)
+        return P_, q_, k_, v_, W2_, xp, xc, P_.keep_frames(xp, xc)
+
+    P, q, k, v, W2, x_prev0, x_curr0, keep = warm_up()
     K, sp = bisect_top_k(P, x_prev0, x_curr0, keep, args.sparsity, ws)
     t_step = M_WARMUP + DT                             # t_p^(1) = 22
+    lpt_info = None
+    if args.lpt and ws > 1 and not args.ulysses:
+        # LPT head assignment by the predicted mask nnz of every head (K4 time is proportional to it): all
+        # ranks' per-head nnz are gathered, heads are re-dealt greedily, and each rank redoes its warm-up
+        import torch.distributed as dist
+        rp0, _ = P.predict_block_mask(x_prev0, x_curr0, M_WARMUP - 1, M_WARMUP, t_step, keep, top_k=K)
+        nnz_local = torch.zeros(H, dtype=torch.float64, device="cpu" if DIST_BACKEND == "gloo" else "cuda")
+        for i, h in enumerate(heads):
+            nnz_local[h] = float(rp0[0, i, -1].item())
+        dist.all_reduce(nnz_local, op=dist.ReduceOp.SUM)
+        cost = nnz_local.cpu().tolist()
+        assign = lpt_head_assignment(cost, ws)
+        loads = [sum(cost[h] for h in a) for a in assign]
+        even = [sum(cost[h] for h in range(*head_range(H, ws, r))) for r in range(ws)]
+        lpt_info = {"max_over_mean_load": round(max(loads) / (sum(loads) / ws), 4),
+                    "contiguous_max_over_mean_load": round(max(even) / (sum(even) / ws), 4)}
+        heads = assign[rank]
+        del P, q, k, v, W2
+        P, q, k, v, W2, x_prev0, x_curr0, keep = warm_up()
+    Hl = len(heads)
+    w = w_full.with_heads(Hl)
+    hist = W2.clone()                                  # A_hat^(t_p^(0)) = A^(m) (P:323)
     xs_prev, xs_curr = x_prev0.clone(), x_curr0.clone()
     rp, ci = P.empty_mask()
     o = torch.empty_like(q)
@@ -260,12 +288,44 @@ def run_ours(args):
     q8 = args.precision == "q8"
     if q8 and exact:
         raise SystemExit("--precision q8 with --stat exact is not supported (the exact statistic needs the bf16 lse)")
+    if args.ulysses and (q8 or exact):
+        raise SystemExit("--ulysses runs the bf16 pooled step")
     qbuf = P.quant_buffer() if q8 else None
 
+    upipe = None
+    if args.ulysses:
+        from paper_2601_11641_b200.parallel import UlyssesChunkPipeline
+        Ns = N // ws
+        qs, ks, vs = syn.family_s_seq_shard(w_full, rank * Ns, (rank + 1) * Ns, step=M_WARMUP, seed=syn.SEED_BASE,
+                                            device="cuda")
+        o_seq = torch.empty_like(qs)
+        upipe = UlyssesChunkPipeline(w_full, chunks_u, **plan_kw)
+        assert [h for c in range(chunks_u) for h in upipe.heads(c)] == heads
+        hlc = upipe.hl
+        uev = []
+
+        def chunk_step(plan, c, qc, kc, vc, oc):
+            sl = slice(c * hlc, (c + 1) * hlc)
+            st_ = torch.cuda.current_stream()
+            e_ = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            e_[0].record(st_)
+            plan.predict_block_mask(x_prev0[:, sl], x_curr0[:, sl], M_WARMUP - 1, M_WARMUP, t_step, keep[:, sl],
+                                    top_k=K, out=(rp[:, sl], ci[:, sl]))
+            e_[1].record(st_)
+            plan.block_sparse_attn_fwd(qc, kc, vc, rp[:, sl], ci[:, sl], out=oc, lse=lse[:, sl])
+            e_[2].record(st_)
+            plan.collect_block_stats(qc, kc, out=Wf[:, sl])
+            plan.update_online_mask(Wf[:, sl], rp[:, sl], ci[:, sl], hist[:, sl], xs_prev[:, sl], xs_curr[:, sl])
+            e_[3].record(st_)
+            uev.append(e_)
+
     def step(timed_kernels=False):
-        if seq is not None:
-            for dst, src in zip((q, k, v), seq):
-                seq_to_heads(src, out=dst)
+        if upipe is not None:
+            uev.clear()
+            upipe.run(qs, ks, vs, o_seq, chunk_step)
+            if timed_kernels:
+                ev["ulysses"] = ev.get("ulysses", []) + [list(uev)]
+            return
         if timed_kernels:
             e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
             e[0].record(stream)
@@ -284,14 +344,14 @@ def run_ours(args):
         else:
             P.collect_block_stats(q, k, out=Wf)
         P.update_online_mask(Wf, rp, ci, hist, xs_prev, xs_curr)
-        if seq is not None:
-            step.o_seq = heads_to_seq(o, out=step.o_seq if getattr(step, "o_seq", None) is not None else None)
         if timed_kernels:
             e[3].record(stream)
             ev["attn"].append((e[1], e[2]))
             ev["rest"].append((e[0], e[1], e[2], e[3]))
 
     launches_per_step = 3 + (4 if q8 else 1) + (1 if exact else 3) + 6   # predict (3) + attn (+3 quantize) + statistic (pool, score, norm) + update (6)
+    if upipe is not None:   # per chunk: the step + 3 packs / unpacks in, 1 pack + 1 unpack out
+        launches_per_step = chunks_u * (launches_per_step + 6 + 2)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -313,9 +373,14 @@ def run_ours(args):
     barrier(ws)
     ms_local = e0.elapsed_time(e1) / args.steps
     ms = max_over_ranks(ms_local, ws)
-    attn_ms = statistics.mean(a.elapsed_time(b) for a, b in ev["attn"])
-    pred_ms = statistics.mean(a.elapsed_time(b) for a, b, _, _ in ev["rest"])
-    upd_ms = statistics.mean(c.elapsed_time(d) for _, _, c, d in ev["rest"])
+    if upipe is not None:   # per step: sum over the chunks' events
+        attn_ms = statistics.mean(sum(e_[1].elapsed_time(e_[2]) for e_ in st_) for st_ in ev["ulysses"])
+        pred_ms = statistics.mean(sum(e_[0].elapsed_time(e_[1]) for e_ in st_) for st_ in ev["ulysses"])
+        upd_ms = statistics.mean(sum(e_[2].elapsed_time(e_[3]) for e_ in st_) for st_ in ev["ulysses"])
+    else:
+        attn_ms = statistics.mean(a.elapsed_time(b) for a, b in ev["attn"])
+        pred_ms = statistics.mean(a.elapsed_time(b) for a, b, _, _ in ev["rest"])
+        upd_ms = statistics.mean(c.elapsed_time(d) for _, _, c, d in ev["rest"])
     attn_ms_max = max_over_ranks(attn_ms, ws)
     value = flops_all / (ms * 1e-3) / 1e12
     attn_tflops = flops_local / (attn_ms * 1e-3) / 1e12
@@ -349,9 +414,10 @@ def run_ours(args):
     # Ulysses variants run serially (upload, step, download on one stream).
     e2e = None
     if not args.no_e2e:
-        hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
+        src = (qs, ks, vs) if upipe is not None else (q, k, v)
+        hq, hk, hv = (t.cpu().pin_memory() for t in src)
         ho = torch.empty_like(hq).pin_memory()
-        pipelined = not (q8 or exact or seq is not None) and w.batch == 1
+        pipelined = not (q8 or exact or upipe is not None) and w.batch == 1
         if pipelined:
             from paper_2601_11641_b200.pipeline import HeadChunkPipeline
             want = args.e2e_chunks
@@ -378,6 +444,12 @@ def run_ours(args):
         for _ in range(args.steps):
             if pipelined:
                 pipe.run(hq, hk, hv, ho, chunk_step)
+            elif upipe is not None:
+                qs.copy_(hq, non_blocking=True)
+                ks.copy_(hk, non_blocking=True)
+                vs.copy_(hv, non_blocking=True)
+                step()
+                ho.copy_(o_seq, non_blocking=True)
             else:
                 q.copy_(hq, non_blocking=True)
                 k.copy_(hk, non_blocking=True)
@@ -426,7 +498,10 @@ def run_ours(args):
                    "target_sparsity": args.sparsity, "nnz_blocks_rank0": nnz_local,
                    "step": "predict(K2b) + attn(K4) + stats(K1) + update(K3: Eq.5 + fit K2a + roll) at t_p=22",
                    "l2": "inputs larger than L2 (Q,K,V = %.2f GB per rank > 126 MB)" % (3 * q.numel() * 2 / 1e9),
-                   "parallelism": (f"ulysses a2a + head-parallel x{ws}" if args.ulysses else f"head-parallel x{ws}")},
+                   "parallelism": (f"ulysses a2a in {chunks_u} overlapped head chunks + head-parallel x{ws}"
+                                   if args.ulysses else
+                                   (f"head-parallel x{ws} (LPT by mask nnz)" if lpt_info else f"head-parallel x{ws}")),
+                   **({"lpt": lpt_info} if lpt_info else {})},
         "attn_ms": round(attn_ms_max, 3), "attn_tflops": round(attn_tflops, 1),
         "attn_pct_bf16_peak": round(100 * attn_tflops / burst, 1),
         "pipeline_overhead_ms": {"predict": round(pred_ms, 4), "stats_update": round(upd_ms, 4)},
@@ -606,6 +681,10 @@ def main():
                     help="K4 schedule (include/moddit.h mod_attn_kernel); default is the headline kernel")
     ap.add_argument("--ulysses", action="store_true",
                     help="sequence-sharded inputs: Ulysses all-to-all in and out of every step (config 5)")
+    ap.add_argument("--ulysses-chunks", type=int, default=0,
+                    help="head chunks of the overlapped Ulysses exchange (0: up to 3 that divide H / P)")
+    ap.add_argument("--lpt", action="store_true",
+                    help="head-parallel: deal heads to ranks by longest-processing-time on the predicted mask nnz")
     args = ap.parse_args()
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
         _self_launch(args.gpus)

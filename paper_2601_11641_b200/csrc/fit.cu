@@ -37,7 +37,8 @@ __global__ void __launch_bounds__(256) project_kernel(const float* __restrict__ 
   const int i0 = tile * rows, i1 = min(i0 + rows, n), R = i1 - i0;
   const size_t start = (bh * n + i0) * (size_t)n;     // first element of the tile (contiguous rows)
   const size_t count = (size_t)R * n;
-  const int shift = (int)(start & 3);                 // so that 16-byte global chunks land 16-byte aligned
+  // so that 16-byte global chunks land 16-byte aligned (U itself may be a head slice: use the address)
+  const int shift = (int)((reinterpret_cast<uintptr_t>(U + start) >> 2) & 3);
   float* t = tile_raw + 4 + shift;                    // t[i * n + j] = U[bh][i0 + i][j]; tile_raw[0..3] pad
   const float* src = U + start;
   const size_t head = min(count, (size_t)((4 - shift) & 3));    // scalars before the first aligned chunk

@@ -584,3 +584,19 @@ def test_plan_solver_chain_degenerate_layout(M, w):
 def test_plan_solver_chain_video_layouts_stay_cholesky(M, w):
     P = plan_for(M, w)
     assert P.solver == "cholesky" and P.min_pivot > 1e-4 and P.create_ms > 0
+
+
+def test_fit_and_update_on_head_slices_of_odd_n(M):
+    """K2a / K3 on head slices of a larger stats tensor (the head-chunk pipelines pass views): with odd n
+    the slices start at addresses that are not 16-byte aligned; results must equal the contiguous copy's
+    bit for bit."""
+    w = syn.Workload("odd-n", 1, 3, 64, 0, 4, 9, 16, 64)     # N = 576, n = 9
+    L = olayout(w)
+    assert L.n % 2 == 1
+    P1 = plan_for(M, w.with_heads(1))
+    U = syn.random_stats(1, 3, L.n, seed=23, device="cuda")
+    for h in range(3):
+        xa = P1.fit_mixture(U[:, h:h + 1])
+        xb = P1.fit_mixture(U[:, h:h + 1].clone())
+        torch.cuda.synchronize()
+        assert torch.equal(xa, xb), h
