@@ -400,7 +400,7 @@ struct Attn1Cfg {
 #define K4_EMU1 2
 #endif
   static constexpr int EMU = K4_EMU;                  // pairs of every 8 exponentiated on the FMA pipe
-  static constexpr int EMU1 = K4_EMU1;                // the same on the PV warp's sub-partition (quarter 1)
+  static constexpr int EMU1 = K4_EMU1;                // the same on the MMA issuers' sub-partitions (quarters 1, 2)
   static constexpr float OVF = 1048576.0f;            // 2^20: half-row sum bound of the lazy reference
 };
 
@@ -657,7 +657,7 @@ __global__ void __launch_bounds__(Attn1Cfg<D, BN>::THREADS, 1)
       if constexpr (C::EMU1 == C::EMU)   // one copy of the loop body (instruction-cache footprint)
         sum = exp_pack<C::EMU, COLS>(s, scale_log2, m_run, pk);
       else
-        sum = quarter == 1 ? exp_pack<C::EMU1, COLS>(s, scale_log2, m_run, pk)
+        sum = (quarter == 1 || quarter == C::S_WARP % 4) ? exp_pack<C::EMU1, COLS>(s, scale_log2, m_run, pk)
                            : exp_pack<C::EMU, COLS>(s, scale_log2, m_run, pk);
       const bool need = !(sum <= C::OVF);
       if (tr) K4T(trole, 3, j);
@@ -894,7 +894,7 @@ __global__ void __launch_bounds__(320, 1)
           const uint64_t bd = smem_desc_sw128(sv + kk * 2048, C::KV_BOX, 1024);
           mma_ts(tmem + C::TMEM_O + X * D, p_t + kk * 8, bd, C::IDESC_O, (np > 0 || kk > 0) ? 1u : 0u);
         }
-        mma_commit(&o_done[X]);
+        if (np + 1 == (X ? LB : LA)) mma_commit(&o_done[X]);   // only the tile's last PV is waited (epilogue)
         const int left = s ? --vrem1 : --vrem0;
         if (left == 0) mma_commit(&v_empty[s]);
         if (X) { pend1 = -1; ++npv1; } else { pend0 = -1; ++npv0; }
@@ -1031,7 +1031,7 @@ __global__ void __launch_bounds__(320, 1)
       const bool valid = row < min(BN, N - q_row0);
       const size_t grow = (size_t)bh * N + q_row0 + row;
       if (LX > 0) {
-        mbar_wait(&o_done[X], (LX - 1) & 1);
+        mbar_wait(&o_done[X], 0);   // committed once, after the tile's last PV
         tc_fence_after();
         const float inv = 1.0f / l_run;
 #pragma unroll

@@ -54,9 +54,11 @@ def timed(fn, reps=20):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="hunyuanvideo-720p", choices=sorted(syn.CONFIGS))
+    ap.add_argument("--drift", type=float, default=0.0,
+                    help="Family S pattern-strength drift over the denoising steps (synthetic/__init__.py)")
     args = ap.parse_args()
     torch.cuda.set_device(0)
-    gen = dict(seed=syn.SEED_BASE, device="cuda")
+    gen = dict(seed=syn.SEED_BASE, device="cuda", drift=args.drift)
     _, _, hbm, _ = load_peaks()
 
     for name in ("tiny", "cogvideox-5b", "wan2.1-14b-720p", "hunyuanvideo-720p"):
@@ -66,7 +68,7 @@ def main():
         P = Plan(w)
         q, k, _ = syn.family_s(w, step=M_WARMUP, **gen)
         _, nae = P.fit_mixture(P.collect_block_stats(q, k), want_nae=True)
-        print(json.dumps({"part": "nae", "config": name, "tokens": w.tokens, "n": P.n, "p": P.p,
+        print(json.dumps({"drift": args.drift, "part": "nae", "config": name, "tokens": w.tokens, "n": P.n, "p": P.p,
                           "nae": summary(nae.double().cpu().numpy())}), flush=True)
         del q, k
 
@@ -79,7 +81,7 @@ def main():
         fits[t] = P.fit_mixture(maps[t])
         del q, k
     der = {t: P.map_rel_error(maps[t], maps[M_WARMUP]).cpu().numpy().ravel() for t in range(M_WARMUP + 1, T_TOTAL + 1)}
-    print(json.dumps({"part": "der", "config": args.config,
+    print(json.dumps({"drift": args.drift, "part": "der", "config": args.config,
                       "der_mean_over_heads": {t: round(float(v.mean()), 6) for t, v in der.items()},
                       "der_max": float(max(v.max() for v in der.values()))}), flush=True)
 
@@ -95,7 +97,7 @@ def main():
         P.update_online_mask(maps[tp], rp, ci, hist, xp, xc)
         tprev, tcurr = tcurr, tp
         rec[tp] = summary(P.map_rel_error(hist, maps[tp]).cpu().numpy())
-    print(json.dumps({"part": "recon", "config": args.config, "top_k": K, "block_sparsity": round(sp, 4),
+    print(json.dumps({"drift": args.drift, "part": "recon", "config": args.config, "top_k": K, "block_sparsity": round(sp, 4),
                       "nre_vs_fresh_full_map": rec}), flush=True)
 
     # linearity of the true fits over (22, 32] against the Eq. 6 line through X^(12), X^(22)
@@ -103,7 +105,7 @@ def main():
     traj = torch.stack([fits[t] for t in ts]).contiguous()
     nre = P.linearity_nre(fits[M_WARMUP], fits[M_WARMUP + DT], M_WARMUP, M_WARMUP + DT, traj, ts).cpu().numpy()
     fin = nre[np.isfinite(nre)]
-    print(json.dumps({"part": "linearity", "config": args.config, "window": [ts[0] - 1, ts[-1]],
+    print(json.dumps({"drift": args.drift, "part": "linearity", "config": args.config, "window": [ts[0] - 1, ts[-1]],
                       "patterns": int(nre.size), "nre": summary(nre),
                       "frac_strong_linearity_lt_0.1": round(float((fin < 0.1).mean()), 4) if fin.size else None}),
           flush=True)
@@ -115,7 +117,7 @@ def main():
     ms_lin = timed(lambda: P.linearity_nre(fits[M_WARMUP], fits[M_WARMUP + DT], M_WARMUP, M_WARMUP + DT, traj, ts))
     b_rel = 2 * BH * n * n * 4
     b_lin = (2 + len(ts)) * BH * p * 8 + BH * (3 * n - 1) * 8
-    print(json.dumps({"part": "timing", "config": args.config,
+    print(json.dumps({"drift": args.drift, "part": "timing", "config": args.config,
                       "map_rel_error_us": round(ms_rel * 1e3, 1), "map_rel_error_gbs": round(b_rel / ms_rel / 1e6, 1),
                       "map_rel_error_bytes": b_rel,
                       "linearity_nre_us": round(ms_lin * 1e3, 1), "linearity_nre_gbs": round(b_lin / ms_lin / 1e6, 1),

@@ -55,6 +55,8 @@ def time_k4(P, q, k, v, rp, ci, reps=10):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="hunyuanvideo-720p", choices=sorted(syn.CONFIGS))
+    ap.add_argument("--drift", type=float, default=0.0,
+                    help="Family S pattern-strength drift over the denoising steps (synthetic/__init__.py)")
     ap.add_argument("--parts", default="sweep,interval,run")
     ap.add_argument("--sparsity", type=float, default=0.878, help="target for interval/run")
     args = ap.parse_args()
@@ -64,7 +66,7 @@ def main():
     burst, sustained, _, _ = load_peaks()
     torch.cuda.set_device(0)
     P = Plan(w, top_k=1, tau_e=0.0)
-    gen = dict(seed=syn.SEED_BASE, device="cuda")
+    gen = dict(seed=syn.SEED_BASE, device="cuda", drift=args.drift)
 
     # warm-up statistics at t = m-1, m (as bench.py) -> fits, keep, K for each target sparsity
     q, k, v = syn.family_s(w, step=M_WARMUP - 1, **gen)
@@ -83,7 +85,7 @@ def main():
             rp, ci = P.predict_block_mask(x_prev, x_curr, M_WARMUP - 1, M_WARMUP, M_WARMUP + DT, keep, top_k=K)
             fl = attn_flops(rp.cpu().numpy(), ci.cpu().numpy(), N, blk, D)
             med, lo, hi = time_k4(P, q, k, v, rp, ci)
-            print(json.dumps({"part": "sweep", "config": args.config, "target_sparsity": target, "top_k": K,
+            print(json.dumps({"drift": args.drift, "part": "sweep", "config": args.config, "target_sparsity": target, "top_k": K,
                               "block_sparsity": round(sp, 4), "tflop": round(fl / 1e12, 3), "k4_ms": round(med, 3),
                               "k4_ms_min": round(lo, 3), "k4_ms_max": round(hi, 3),
                               "tflops": round(fl / med / 1e9, 1), "pct_burst": round(100 * fl / med / 1e9 / burst, 1),
@@ -141,7 +143,7 @@ def main():
                 del qt, kt, vt
             tot = sum(calls.values())
             over = tot - calls["attn"]
-            print(json.dumps({"part": "interval", "config": args.config, "window": [win[0] - 1, win[-1]],
+            print(json.dumps({"drift": args.drift, "part": "interval", "config": args.config, "window": [win[0] - 1, win[-1]],
                               "top_k": K, "block_sparsity": round(sp, 4),
                               "schedule_interval_ms": round(sum(per_step[t - 1] for t in win), 3),
                               "replay_ms": {key: round(x, 3) for key, x in calls.items()},
@@ -153,7 +155,7 @@ def main():
             dense_total = sum(per_step[t - 1] for t in range(1, M_WARMUP + 1))
             sparse_total = sum(per_step[t - 1] for t in range(M_WARMUP + 1, T_TOTAL + 1))
             all_dense = T_TOTAL * dense_ms
-            print(json.dumps({"part": "run", "config": args.config, "T": T_TOTAL, "m": M_WARMUP, "dt": DT,
+            print(json.dumps({"drift": args.drift, "part": "run", "config": args.config, "T": T_TOTAL, "m": M_WARMUP, "dt": DT,
                               "top_k": K, "block_sparsity": round(sp, 4),
                               "warmup_ms": round(dense_total, 1), "sparse_steps_ms": round(sparse_total, 1),
                               "schedule_total_ms": round(dense_total + sparse_total, 1),
