@@ -399,8 +399,13 @@ struct Attn1Cfg {
 #ifndef K4_EMU1
 #define K4_EMU1 2
 #endif
-  static constexpr int EMU = K4_EMU;                  // pairs of every 8 exponentiated on the FMA pipe
-  static constexpr int EMU1 = K4_EMU1;                // the same on the MMA issuers' sub-partitions (quarters 1, 2)
+#ifndef K4_EMU_D64
+#define K4_EMU_D64 K4_EMU
+#endif
+  // pairs of every 8 exponentiated on the FMA pipe (the rest on MUFU); D = 64 has half the tensor work per
+  // block, so its softmax can move more of the exponentials off MUFU
+  static constexpr int EMU = D == 64 ? K4_EMU_D64 : K4_EMU;
+  static constexpr int EMU1 = D == 64 ? K4_EMU_D64 : K4_EMU1;   // the same on the MMA issuers' sub-partitions
   static constexpr float OVF = 1048576.0f;            // 2^20: half-row sum bound of the lazy reference
 };
 
