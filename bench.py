@@ -677,7 +677,7 @@ def main():
     ap.add_argument("--stat", default="pooled", choices=["pooled", "exact"],
                     help="block statistic: pooled (north_star (1)) or the paper's exact Eq. 2 (SURVEY f1)")
     ap.add_argument("--eta", type=float, default=1e-4)
-    ap.add_argument("--attn-kernel", default="default", choices=["default", "splitkv", "pair"],
+    ap.add_argument("--attn-kernel", default="default", choices=["default", "splitkv", "pair", "wide"],
                     help="K4 schedule (include/moddit.h mod_attn_kernel); default is the headline kernel")
     ap.add_argument("--ulysses", action="store_true",
                     help="sequence-sharded inputs: Ulysses all-to-all in and out of every step (config 5)")

@@ -73,9 +73,12 @@ typedef enum {
 /* K4 kernel schedule (all compute the same Eq. 1 result; parity-tested alike).  DEFAULT is the one
  * bench.py times; the others are kept for A/B measurement. */
 typedef enum {
-  MOD_ATTN_DEFAULT = 0,     /* one 8-warp softmax group over column halves, NS S buffers ahead of it */
+  MOD_ATTN_DEFAULT = 0,     /* D = 128 (or 64-token blocks): 8 free-running softmax warps of 16 rows, NS S
+                               buffers ahead of them, MMA issue split over two warps; D = 64 with 128-token
+                               blocks: the WIDE schedule (measured faster there) */
   MOD_ATTN_SPLITKV = 1,     /* two 4-warp softmax groups splitting the index list (round-1 kernel) */
-  MOD_ATTN_PAIR = 2         /* two query blocks per CTA walking their merged index list (f4) */
+  MOD_ATTN_PAIR = 2,        /* two query blocks per CTA walking their merged index list (f4) */
+  MOD_ATTN_WIDE = 3         /* 16 softmax warps, split-KV over the two key halves of each block (128-token blocks) */
 } mod_attn_kernel;
 
 typedef struct {

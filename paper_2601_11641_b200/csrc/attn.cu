@@ -751,6 +751,312 @@ __global__ void __launch_bounds__(Attn1Cfg<D, BN>::THREADS, 1)
 }
 
 // ================================================================================================
+// Wide K4 schedule (MOD_ATTN_WIDE, 128-token blocks): FOUR softmax warps per SM sub-partition.
+// ncu of the default schedule shows ~0.7 eligible warps per scheduler and 50 % issue utilisation: the
+// softmax is latency-bound with two warps per sub-partition.  Here warp (quarter q, half h, key half c)
+// owns the 16 rows [32q + 16h, +16) and the 64 keys [64c, +64) of every block (32 per thread, the two
+// 32-key chunks of a row in lanes t and t ^ 16), i.e. a split-KV over the two key halves of each block:
+// key half c has its own reference max, row sums and accumulator O_c, so no warp ever waits for another
+// until the epilogue merges (m_c, l_c, O_c).  P of key half c is written over the first 32 columns of
+// that half's own S columns (no cross-warp overlap); PV^c accumulates into O_c from those columns.
+// TMEM: S[b] for b < NS, then O_0, O_1 (NS = 2 at D = 128, 3 at D = 64).  608 threads: producer,
+// PV issuer, 16 softmax warps, S issuer.
+template <int D, int BN>
+struct WideCfg {
+  static constexpr int BM = 128;
+  static constexpr int NS = (512 - 2 * D) / BN > 7 ? 7 : (512 - 2 * D) / BN;
+  static constexpr int VSTAGES = 2;
+  static constexpr int KH = BN / 2;                   // keys per key half
+  static constexpr int COLS = KH / 2;                 // score columns per thread
+  static constexpr int Q_BOX = BM * 128, KV_BOX = BN * 128, NATOM = D / 64;
+  static constexpr int Q_BYTES = Q_BOX * NATOM, KV_BYTES = KV_BOX * NATOM;
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = OFF_Q + Q_BYTES;
+  static constexpr int OFF_V = OFF_K + NS * KV_BYTES;
+  static constexpr int OFF_BAR = OFF_V + VSTAGES * KV_BYTES;
+  // q_full, k_full[NS], v_full[2], s_full[NS], p_full[NS][2], o_done[NS]
+  static constexpr int NUM_BARS = 1 + NS + VSTAGES + NS + 2 * NS + NS;
+  static constexpr int OFF_XCH = (OFF_BAR + NUM_BARS * 8 + 16 + 15) / 16 * 16;
+  static constexpr int SMEM = OFF_XCH + 2 * 2 * 128 * 4;   // epilogue (m, l) per key half per row
+  static constexpr int TMEM_O = NS * BN;              // O_c at TMEM_O + c * D
+  static constexpr uint32_t TMEM_COLS = (NS * BN + 2 * D) <= 256 ? 256 : 512;
+  static constexpr uint32_t IDESC_S = idesc_bf16_f32(BM, BN, false, false);
+  static constexpr uint32_t IDESC_O = idesc_bf16_f32(BM, D, false, true);
+  static constexpr int SOFTMAX_WARPS = 16;
+  static constexpr int S_WARP = 2 + SOFTMAX_WARPS;
+  static constexpr int THREADS = 64 + 32 * SOFTMAX_WARPS + 32;
+  static constexpr int EMU = K4_EMU;
+  static constexpr float OVF = 1048576.0f;
+};
+
+template <int D, int BN>
+__global__ void __launch_bounds__(WideCfg<D, BN>::THREADS, 1)
+    attn_wide_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                     const __grid_constant__ CUtensorMap tm_v, const int* __restrict__ row_ptr,
+                     const int* __restrict__ col_idx, __nv_bfloat16* __restrict__ out, float* __restrict__ lse,
+                     int N, int n, int block, float scale_log2) {
+  using C = WideCfg<D, BN>;
+  constexpr int NS = C::NS;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = bars + 1;
+  uint64_t* v_full = k_full + NS;
+  uint64_t* s_full = v_full + C::VSTAGES;
+  uint64_t* p_full = s_full + NS;        // [b * 2 + c]
+  uint64_t* o_done = p_full + 2 * NS;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + NS);
+  float* xch = reinterpret_cast<float*>(smem + C::OFF_XCH);   // [c][m|l][row]
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0 && (smem_u32(smem) & 1023u) != 0) __trap();
+  const int item = blockIdx.x;
+  const int bh = item / n, qi = item % n;
+  const int beg = row_ptr[(size_t)bh * (n + 1) + qi];
+  const int L = row_ptr[(size_t)bh * (n + 1) + qi + 1] - beg;
+  const int* cols = col_idx + (size_t)bh * n * n + beg;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&s_full[s], 1);
+      mbar_init(&p_full[2 * s], C::SOFTMAX_WARPS / 2);
+      mbar_init(&p_full[2 * s + 1], C::SOFTMAX_WARPS / 2);
+      mbar_init(&o_done[s], 1);
+    }
+    for (int s = 0; s < C::VSTAGES; ++s) mbar_init(&v_full[s], 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const uint64_t pol_q = policy_evict_first(), pol_kv = policy_evict_last();
+  auto load_k = [&](int j) {
+    const int s = j % NS;
+    unsigned char* dst = smem + C::OFF_K + s * C::KV_BYTES;
+    mbar_arrive_expect_tx(&k_full[s], C::KV_BYTES);
+    const int row = cols[j] * block;
+#pragma unroll
+    for (int a = 0; a < C::NATOM; ++a) tma_load_3d(dst + a * C::KV_BOX, &tm_k, &k_full[s], a * 64, row, bh, pol_kv);
+  };
+  auto load_v = [&](int j) {
+    const int s = j & 1;
+    unsigned char* dst = smem + C::OFF_V + s * C::KV_BYTES;
+    mbar_arrive_expect_tx(&v_full[s], C::KV_BYTES);
+    const int row = cols[j] * block;
+#pragma unroll
+    for (int a = 0; a < C::NATOM; ++a) tma_load_3d(dst + a * C::KV_BOX, &tm_v, &v_full[s], a * 64, row, bh, pol_kv);
+  };
+  auto issue_s = [&](int j, auto bc) {
+    constexpr int b = decltype(bc)::value;
+    K4_WAIT(&k_full[b], (j / NS) & 1);
+    tc_fence_after();
+    const uint64_t a_base = smem_desc_sw128(smem_u32(smem + C::OFF_Q), 16, 1024);
+    const uint64_t b_base = smem_desc_sw128(smem_u32(smem + C::OFF_K + b * C::KV_BYTES), 16, 1024);
+    static_for<D / 16>([&](auto kc) {
+      constexpr int kk = decltype(kc)::value;
+      mma_ss_e<((kk / 4) * C::Q_BOX + (kk % 4) * 32) / 16, ((kk / 4) * C::KV_BOX + (kk % 4) * 32) / 16>(
+          tmem + b * BN, a_base, b_base, C::IDESC_S, kk > 0 ? 1u : 0u);
+    });
+    mma_commit_e(&s_full[b]);
+  };
+  // PV^c_j: O_c += P_j[:, keys of half c] V_j[keys of half c, :]; P^c packed in that half's first KH/2 columns
+  auto issue_pv = [&](int j, auto bc, auto vc) {
+    constexpr int b = decltype(bc)::value, vs = decltype(vc)::value;
+    K4T(0, 0, j);
+    K4_WAIT(&v_full[vs], (j >> 1) & 1);
+    K4T(0, 1, j);
+    const uint64_t v_base = smem_desc_sw128(smem_u32(smem + C::OFF_V + vs * C::KV_BYTES), C::KV_BOX, 1024);
+    const uint32_t acc0 = j > 0 ? 1u : 0u;
+    static_for<2>([&](auto cc) {
+      constexpr int c = decltype(cc)::value;
+      K4_WAIT(&p_full[2 * b + c], (j / NS) & 1);
+      tc_fence_after();
+      static_for<C::KH / 16>([&](auto kc) {
+        constexpr int kk = decltype(kc)::value;
+        mma_ts_e<c * C::KH + kk * 8, (c * C::KH / 16 + kk) * 2048 / 16>(tmem + C::TMEM_O + c * D, tmem + b * BN,
+                                                                        v_base, C::IDESC_O, kk > 0 ? 1u : acc0);
+      });
+    });
+    mma_commit_e(&o_done[b]);
+    K4T(0, 2, j);
+    K4T(0, 3, j);
+  };
+  constexpr int UPV = (NS % 2) ? 2 * NS : NS;
+
+  if (warp == 0) {
+    if (lane == 0 && L > 0) {
+      tma_prefetch_desc(&tm_q);
+      tma_prefetch_desc(&tm_k);
+      tma_prefetch_desc(&tm_v);
+      mbar_arrive_expect_tx(q_full, C::Q_BYTES);
+#pragma unroll
+      for (int a = 0; a < C::NATOM; ++a)
+        tma_load_3d(smem + C::OFF_Q + a * C::Q_BOX, &tm_q, q_full, a * 64, qi * block, bh, pol_q);
+      for (int j = 0; j < NS && j < L; ++j) load_k(j);
+      for (int j = 0; j < L; ++j) {
+        if (j >= 2) K4_WAIT(&o_done[(j - 2) % NS], ((j - 2) / NS) & 1);
+        load_v(j);
+        if (j + NS < L) {
+          K4_WAIT(&s_full[j % NS], (j / NS) & 1);
+          load_k(j + NS);
+        }
+      }
+    }
+  } else if (warp == 1 || warp == C::S_WARP) {
+    if (L > 0) {
+      K4_WAIT(q_full, 0);
+      tc_fence_after();
+      if (warp == 1) {
+        for (int j0 = 0; j0 < L; j0 += UPV) {
+          static_for<UPV>([&](auto uc) {
+            constexpr int u = decltype(uc)::value;
+            if (j0 + u < L) issue_pv(j0 + u, std::integral_constant<int, u % NS>{}, std::integral_constant<int, u % 2>{});
+          });
+        }
+      } else {
+        for (int j0 = 0; j0 < L; j0 += NS) {
+          static_for<NS>([&](auto uc) {
+            constexpr int u = decltype(uc)::value;
+            const int j = j0 + u;
+            if (j < L) {
+              if (j >= NS) {
+                K4_WAIT(&o_done[u], ((j - NS) / NS) & 1);
+                tc_fence_after();
+              }
+              issue_s(j, uc);
+            }
+          });
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ softmax: warp (quarter, row half, key half)
+    constexpr int COLS = C::COLS, KH = C::KH;
+    constexpr unsigned FULL = 0xffffffffu;
+    const int quarter = warp & 3;
+    const int g = (warp - 2) >> 2;
+    const int h = g & 1, c = g >> 1;
+    const int colq = lane >> 4;
+    const int row = quarter * 32 + h * 16 + (lane & 15);
+    const uint32_t lane_off = (uint32_t)(quarter * 32 + h * 16) << 16;
+    const int q_row0 = qi * block;
+    const int q_rows = min(block, N - q_row0);
+    float m_run = -INFINITY, l_run = 0.f;   // this key half's reference max (log2, scaled) / this thread's sum
+    int col_next = L > 0 ? cols[0] : 0;
+#pragma unroll 1
+    for (int j = 0; j < L; ++j) {
+      const int b = j % NS;
+      const int col = col_next;
+      if (j + 1 < L) col_next = cols[j + 1];
+      mbar_wait(&s_full[b], (j / NS) & 1);
+      tc_fence_after();
+      uint32_t sr[COLS];
+      tmem_ld_rows<COLS, COLS>(tmem + lane_off + b * BN + c * KH, sr);   // keys c*KH + colq*COLS + [0, COLS)
+      tmem_ld_wait();
+      float* s = reinterpret_cast<float*>(sr);
+      const int kv_valid = N - col * block - c * KH - colq * COLS;
+      if (kv_valid < COLS) {
+#pragma unroll
+        for (int e = 0; e < COLS; ++e)
+          if (e >= kv_valid) s[e] = -INFINITY;
+      }
+      if (__any_sync(FULL, m_run == -INFINITY)) {
+        // no finite score of this key half seen yet (first block, or a fully masked ragged half): exact max
+        const float mx = row_max<COLS>(s) * scale_log2;
+        const float mxp = fmaxf(mx, __shfl_xor_sync(FULL, mx, 16));
+        if (m_run == -INFINITY) m_run = mxp;
+      }
+      const float m_e = m_run == -INFINITY ? 0.f : m_run;   // all scores -inf so far: p = 0 for any finite m
+      uint32_t pk[COLS / 2];
+      float sum = exp_pack<C::EMU, COLS>(s, scale_log2, m_e, pk);
+      const bool need = !(sum <= C::OVF);
+      if (__any_sync(FULL, need)) {
+        const int need_peer = __shfl_xor_sync(FULL, (int)need, 16);
+        const bool need_row = need || need_peer != 0;
+        float rmax = row_max<COLS>(s) * scale_log2;
+        rmax = fmaxf(rmax, __shfl_xor_sync(FULL, rmax, 16));
+        const float m_new = need_row ? fmaxf(m_e, rmax) : m_e;
+        const float alpha = ex2(m_e - m_new);
+        if (need_row) sum = exp_pack<0, COLS>(s, scale_log2, m_new, pk);
+        l_run *= alpha;
+        m_run = m_new;
+        if (j > 0 && __any_sync(FULL, alpha < 1.f)) {
+          mbar_wait(&o_done[(j - 1) % NS], ((j - 1) / NS) & 1);   // PV_{j-1} (both halves) has written O
+          tc_fence_after();
+          constexpr int OH = D / 2, OCH = OH < 32 ? OH : 32;
+#pragma unroll
+          for (int k = 0; k < OH / OCH; ++k) {
+            uint32_t o[OCH];
+            tmem_ld_rows<OCH, OH>(tmem + lane_off + C::TMEM_O + c * D + k * OCH, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < OCH; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+            tmem_st_rows<OCH, OH>(tmem + lane_off + C::TMEM_O + c * D + k * OCH, o);
+          }
+        }
+      }
+      l_run += sum;
+      tmem_st_rows<COLS / 2, COLS / 2>(tmem + lane_off + b * BN + c * KH, pk);   // P^c over its half's columns
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[2 * b + c]);
+    }
+    // epilogue: merge the two key halves' (m_c, l_c, O_c); warp c writes O columns [c D/2, (c+1) D/2)
+    const float l_c = l_run + __shfl_xor_sync(FULL, l_run, 16);
+    auto red = reinterpret_cast<float(*)[2][128]>(xch);   // [c][m|l][row]
+    if (lane < 16) {
+      red[c][0][row] = m_run;
+      red[c][1][row] = l_c;
+    }
+    named_bar_sync(1 + quarter * 2 + h, 64);   // the two key-half warps of these 16 rows
+    const float m0 = red[0][0][row], l0 = red[0][1][row], m1 = red[1][0][row], l1 = red[1][1][row];
+    const float m = fmaxf(m0, m1);
+    const float f0 = m0 == -INFINITY ? 0.f : ex2(m0 - m), f1 = m1 == -INFINITY ? 0.f : ex2(m1 - m);
+    const float l = l0 * f0 + l1 * f1;
+    const bool valid = row < q_rows;
+    const size_t grow = (size_t)bh * N + q_row0 + row;
+    constexpr int OQ = D / 4;               // O columns per thread
+    if (L > 0) {
+      mbar_wait(&o_done[(L - 1) % NS], ((L - 1) / NS) & 1);
+      tc_fence_after();
+      const float a0 = f0 / l, a1 = f1 / l;
+      uint32_t o0[OQ], o1[OQ];
+      tmem_ld_rows<OQ, OQ>(tmem + lane_off + C::TMEM_O + c * (D / 2), o0);
+      tmem_ld_rows<OQ, OQ>(tmem + lane_off + C::TMEM_O + D + c * (D / 2), o1);
+      tmem_ld_wait();
+      uint32_t pkd[OQ / 2];
+#pragma unroll
+      for (int e = 0; e < OQ / 2; ++e)
+        pkd[e] = pack_bf16(fmaf(__uint_as_float(o1[2 * e]), a1, __uint_as_float(o0[2 * e]) * a0),
+                           fmaf(__uint_as_float(o1[2 * e + 1]), a1, __uint_as_float(o0[2 * e + 1]) * a0));
+      if (valid) {
+        int4* dst = reinterpret_cast<int4*>(out + grow * D + c * (D / 2) + colq * OQ);
+#pragma unroll
+        for (int e = 0; e < OQ / 8; ++e) dst[e] = make_int4(pkd[4 * e], pkd[4 * e + 1], pkd[4 * e + 2], pkd[4 * e + 3]);
+      }
+      if (valid && lse && c == 0 && colq == 0) lse[grow] = (m + __log2f(l)) * 0.69314718055994531f;
+    } else if (valid) {
+      int4* dst = reinterpret_cast<int4*>(out + grow * D + c * (D / 2) + colq * OQ);
+#pragma unroll
+      for (int e = 0; e < OQ / 8; ++e) dst[e] = make_int4(0, 0, 0, 0);
+      if (lse && c == 0 && colq == 0) lse[grow] = -INFINITY;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<C::TMEM_COLS>(tmem);
+  }
+}
+
+// ================================================================================================
 // Paired query blocks: one CTA per (b, h, pair of query blocks 2p, 2p+1).
 // Adjacent rows of the MOD-DiT mask share most of their index lists (vertical columns, frame
 // squares, diagonals whose neighbour offset is also selected: 79 % at Hunyuan 720p, Family S), so the
@@ -1125,6 +1431,12 @@ mod_status launch_default(mod_plan P, const void* q, const void* k, const void* 
 }
 
 template <int D, int BN>
+mod_status launch_wide(mod_plan P, const void* q, const void* k, const void* v, const int* row_ptr,
+                       const int* col_idx, void* o, float* lse, cudaStream_t s) {
+  return launch_rows<WideCfg<D, BN>>(P, attn_wide_kernel<D, BN>, D, BN, q, k, v, row_ptr, col_idx, o, lse, s);
+}
+
+template <int D, int BN>
 mod_status launch_split(mod_plan P, const void* q, const void* k, const void* v, const int* row_ptr,
                         const int* col_idx, void* o, float* lse, cudaStream_t s) {
   return launch_rows<SplitCfg<D, BN>>(P, attn_split_kernel<D, BN>, D, BN, q, k, v, row_ptr, col_idx, o, lse, s);
@@ -1161,6 +1473,12 @@ int effective_kernel(mod_plan P) {
     if (P->L.block == 128 && P->n <= cap && P->n <= 65535) return MOD_ATTN_PAIR;
     return MOD_ATTN_DEFAULT;
   }
+  if (want == MOD_ATTN_WIDE) return P->L.block == 128 ? MOD_ATTN_WIDE : MOD_ATTN_DEFAULT;
+  // the default schedule by shape: at D = 64 the tensor work per block halves and the softmax alone bounds
+  // the kernel; the wide schedule's four softmax warps per sub-partition hide its latencies better there
+  // (CogVideoX-5B: 598 vs 559 TFLOP/s), while at D = 128 the 8-warp schedule with three S buffers is faster
+  // (1212 vs 1161 TFLOP/s at Hunyuan; profiles/r2/README.md)
+  if (want == MOD_ATTN_DEFAULT && P->L.head_dim == 64 && P->L.block == 128) return MOD_ATTN_WIDE;
   return want;
 }
 }  // namespace
@@ -1183,6 +1501,7 @@ extern "C" const char* mod_attn_kernel_name(mod_plan P) {
       return D == 128 ? (BN == 128 ? "attn_split_kernel<128,128>" : "attn_split_kernel<128,64>")
                       : (BN == 128 ? "attn_split_kernel<64,128>" : "attn_split_kernel<64,64>");
     case MOD_ATTN_PAIR: return D == 128 ? "attn_pair_kernel<128,128>" : "attn_pair_kernel<64,128>";
+    case MOD_ATTN_WIDE: return D == 128 ? "attn_wide_kernel<128,128>" : "attn_wide_kernel<64,128>";
     default:
       return D == 128 ? (BN == 128 ? "attn_fwd_kernel<128,128>" : "attn_fwd_kernel<128,64>")
                       : (BN == 128 ? "attn_fwd_kernel<64,128>" : "attn_fwd_kernel<64,64>");
@@ -1204,6 +1523,10 @@ extern "C" mod_status mod_block_sparse_attn_fwd(mod_plan P, const void* q, const
     case MOD_ATTN_PAIR:
       st = D == 128 ? launch_pair<128>(P, q, k, v, row_ptr, col_idx, o, lse, s)
                     : launch_pair<64>(P, q, k, v, row_ptr, col_idx, o, lse, s);
+      break;
+    case MOD_ATTN_WIDE:
+      st = D == 128 ? launch_wide<128, 128>(P, q, k, v, row_ptr, col_idx, o, lse, s)
+                    : launch_wide<64, 128>(P, q, k, v, row_ptr, col_idx, o, lse, s);
       break;
     case MOD_ATTN_SPLITKV:
       if (D == 128 && BN == 128) st = launch_split<128, 128>(P, q, k, v, row_ptr, col_idx, o, lse, s);

@@ -31,7 +31,7 @@ def M():
     return m
 
 
-KERNELS = ["default", "splitkv", "pair"]
+KERNELS = ["default", "splitkv", "pair", "wide"]
 
 
 @pytest.fixture(params=KERNELS)
