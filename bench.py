@@ -349,7 +349,7 @@ def run_ours(args):
             ev["attn"].append((e[1], e[2]))
             ev["rest"].append((e[0], e[1], e[2], e[3]))
 
-    launches_per_step = 3 + (4 if q8 else 1) + (1 if exact else 3) + 6   # predict (3) + attn (+3 quantize) + statistic (pool, score, norm) + update (6)
+    launches_per_step = 3 + (4 if q8 else 1) + (1 if exact else 4) + 6   # predict (3) + attn (+3 quantize) + statistic (pool, split, 2 score passes) + update (6)
     if upipe is not None:   # per chunk: the step + 3 packs / unpacks in, 1 pack + 1 unpack out
         launches_per_step = chunks_u * (launches_per_step + 6 + 2)
     for _ in range(args.warmup):

@@ -558,9 +558,14 @@ extern "C" mod_status mod_plan_create(const mod_layout* layout, const mod_config
   P->proj_rows = std::max(1, std::min(kProjRows, (kProjSmemFloats - 4) / n));
   P->proj_tiles = (n + P->proj_rows - 1) / P->proj_rows;
   size_t off = 0;
+  // K1 pre-split operand tiles (stats.cu): per head ceil(n/128) tiles of 128 rows x D, bf16 hi + lo
+  const size_t split_bytes = BH * (size_t)((n + 127) / 128) * 128 * L.head_dim * 2 * sizeof(uint16_t);
   P->ws_qbar = off; off = align_up(off + BH * n * L.head_dim * sizeof(float));
   P->ws_kbar = off; off = align_up(off + BH * n * L.head_dim * sizeof(float));
-  P->ws_part = off; off = align_up(off + BH * P->proj_tiles * (size_t)p * sizeof(double));
+  P->ws_qs = off;   off = align_up(off + split_bytes, 1024);
+  P->ws_ks = off;   off = align_up(off + split_bytes, 1024);
+  P->ws_part = off; off = align_up(off + std::max(BH * P->proj_tiles * (size_t)p * sizeof(double),
+                                                  BH * (size_t)n * 4 * 2 * sizeof(float)));   // + K1 (m, l) partials
   P->ws_r = off;    off = align_up(off + BH * (size_t)p * sizeof(double));
   P->ws_x = off;    off = align_up(off + BH * (size_t)p * sizeof(double));
   P->ws_nae = off;  off = align_up(off + 2 * BH * (size_t)n * sizeof(double));

@@ -7,19 +7,34 @@
 //   z_ij   = s * qbar_i . kbar_j                                      (s = 1/sqrt(D))
 //   W_ij   = |I_j| e^{z_ij} / sum_j' |I_j'| e^{z_ij'}                 (block mass; ragged blocks Z16)
 //
-// Three kernels:
-//   pool_kernel   -- HBM-bound: streams Q and K once (2*B*H*N*D*2 bytes) with 128-bit
-//                    non-allocating loads; one CTA per (tensor, head, block); fixed-order
-//                    reduction (deterministic).
-//   score_tc_kernel -- z = qbar kbar^T (n x n x D per head) on tcgen05 with a bf16 hi/lo split of the
-//                    fp32 means (3 MMAs per K step), fused with the log-size bias and per-tile row
-//                    (max, sum) partials; softmax_norm_kernel finishes the row softmax.
+// Four kernels:
+//   pool_kernel   -- HBM-bound: streams Q and K once (2*B*H*N*D*2 bytes) with 128-bit non-allocating
+//                    loads; one CTA per (tensor, head, block); fixed-order reduction (deterministic);
+//   split_kernel  -- the bf16 (hi, lo) split of the means into pre-swizzled 128-row operand tiles;
+//   score_kernel<D, false> / <D, true> -- z = qbar kbar^T on tcgen05 (3 bf16 MMAs per K step from the
+//                    split tiles), pass 0 the rows' (max, sum) partials per column chunk, pass 1 the
+//                    normalised W written once (the MMA is recomputed instead of storing logits).
 #include "common.cuh"
 #include "sm100.cuh"
 
 using namespace sm100;
 
 namespace {
+
+// Pre-split operand tiles of the score MMA, written by pool_kernel: for each 128-row tile t of the n
+// block means of a head, [hi | lo][D/64 atoms][128 rows x 128 bytes] bf16 in exactly the 128B-swizzled
+// K-major shared-memory layout (row r, 16-byte chunk c of an atom at r*128 + ((c ^ (r & 7)) << 4)), so a
+// CTA of the score kernel fetches an operand tile with ONE contiguous bulk copy.  Rows >= n are zero.
+template <int D>
+struct SplitTile {
+  static constexpr int NATOM = D / 64, ATOM = 128 * 128;
+  static constexpr int HALF = NATOM * ATOM;        // bytes of hi (or lo) of one tile
+  static constexpr int BYTES = 2 * HALF;           // hi + lo
+  __device__ static size_t offset(int row, int c16) {   // byte offset inside a tile's hi half
+    const int r = row & 127;
+    return (size_t)(c16 >> 3) * ATOM + r * 128 + (((c16 & 7) ^ (r & 7)) << 4);
+  }
+};
 
 template <int D>
 __global__ void __launch_bounds__(256) pool_kernel(const __nv_bfloat16* __restrict__ q,
@@ -71,175 +86,233 @@ __global__ void __launch_bounds__(256) pool_kernel(const __nv_bfloat16* __restri
   }
 }
 
-// z = s * qbar kbar^T on the tensor cores (north_star: "tensor cores are used ... in the QK^T of the
-// pooled scores"), fused with the log-size bias; the row softmax is split in two passes so that the
-// grid covers every (128-row, 64-column) tile of every head (2 CTAs per SM):
-//   score_tc_kernel  builds the bf16 (hi, lo) split of the fp32 means, hi = bf16(x), lo = bf16(x - hi),
-//                    K-major in the 128B-swizzled layout, one thread issues
-//                    Z = A_hi B_hi^T + A_hi B_lo^T + A_lo B_hi^T (fp32 accumulate in TMEM; the dropped
-//                    lo*lo term is < 2^-16 relative, far inside the 1e-3 bar on W), then thread = row:
-//                    logits v = (s z + ln|I_j|) log2 e -> W, and the tile's (max, sum 2^(v-max)) per row
-//   softmax_norm_kernel  one warp per row: combine the row's tile partials in a fixed order, then
-//                    W = 2^(v - m) / l over the row, coalesced (the logits are L2-resident)
+// fp32 means [BH, n, D] -> the pre-split tiles (SplitTile): one thread per 16-byte chunk of a tile row,
+// hi = bf16(x), lo = bf16(x - hi) (the dropped lo*lo product is < 2^-16 relative); rows >= n are zero.
 template <int D>
-struct ScoreCfg {
-  static constexpr int TM = 128, TN = 64;                  // tile rows (MMA M) / columns (MMA N)
-  static constexpr int NATOM = D / 64;
-  static constexpr int A_ATOM = TM * 128, B_ATOM = TN * 128;
-  static constexpr int A_BYTES = A_ATOM * NATOM, B_BYTES = B_ATOM * NATOM;
-  static constexpr int OFF_AH = 0, OFF_AL = A_BYTES, OFF_BH = 2 * A_BYTES, OFF_BL = 2 * A_BYTES + B_BYTES;
-  static constexpr int OFF_BAR = 2 * A_BYTES + 2 * B_BYTES;
-  static constexpr int SMEM = OFF_BAR + 64 + 1024;          // + alignment slack
-  static constexpr uint32_t IDESC = idesc_bf16_f32(TM, TN, false, false);
-};
-
-// ROWS rows from row0 of a [n, D] fp32 matrix -> bf16 hi / lo tiles (K-major, 128B swizzle).
-// 128 threads; thread t handles 16-byte chunks t, t+128, ... (consecutive threads: consecutive
-// chunks of a row -> coalesced loads); batches of 8 chunks keep 16 independent loads in flight.
-template <int D, int ROWS>
-__device__ __forceinline__ void build_split(const float* __restrict__ src, int row0, int n, unsigned char* hi_tile,
-                                            unsigned char* lo_tile, int atom_bytes, int t) {
-  constexpr int CPR = D / 8;                  // 16-byte (8-element) chunks per row
-  constexpr int PER = ROWS * CPR / 128;       // chunks per thread
-  constexpr int BATCH = PER < 8 ? PER : 8;
+__global__ void __launch_bounds__(256) split_kernel(const float* __restrict__ qbar, const float* __restrict__ kbar,
+                                                     unsigned char* __restrict__ qs, unsigned char* __restrict__ ks,
+                                                     int n, int T, int BH) {
+  using ST = SplitTile<D>;
+  constexpr int CPR = D / 8;
+  const size_t per = (size_t)BH * T * 128 * CPR;
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= 2 * per) return;
+  const bool isk = e >= per;
+  const size_t f = isk ? e - per : e;
+  const int c16 = (int)(f % CPR);
+  const size_t rr = f / CPR;                   // bh * T*128 + row
+  const int row = (int)(rr % ((size_t)T * 128));
+  const size_t bh = rr / ((size_t)T * 128);
+  float x[8];
+  if (row < n) {
+    const float4* src = reinterpret_cast<const float4*>((isk ? kbar : qbar) + (bh * n + row) * D + 8 * c16);
+    const float4 a = __ldg(src), b = __ldg(src + 1);
+    x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+  } else {
 #pragma unroll
-  for (int b0 = 0; b0 < PER; b0 += BATCH) {
-    float4 va[BATCH], vb[BATCH];
-#pragma unroll
-    for (int u = 0; u < BATCH; ++u) {
-      const int e = t + (b0 + u) * 128;
-      const int r = e / CPR, k16 = e % CPR;
-      const bool ok = row0 + r < n;
-      const float4* p = reinterpret_cast<const float4*>(src + (size_t)(row0 + r) * D + k16 * 8);
-      va[u] = ok ? __ldg(p) : make_float4(0.f, 0.f, 0.f, 0.f);
-      vb[u] = ok ? __ldg(p + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-#pragma unroll
-    for (int u = 0; u < BATCH; ++u) {
-      const int e = t + (b0 + u) * 128;
-      const int r = e / CPR, k16 = e % CPR;
-      const float x[8] = {va[u].x, va[u].y, va[u].z, va[u].w, vb[u].x, vb[u].y, vb[u].z, vb[u].w};
-      uint32_t h[4], l[4];
-#pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        const __nv_bfloat16 h0 = __float2bfloat16_rn(x[2 * w]), h1 = __float2bfloat16_rn(x[2 * w + 1]);
-        const __nv_bfloat16 l0 = __float2bfloat16_rn(x[2 * w] - __bfloat162float(h0));
-        const __nv_bfloat16 l1 = __float2bfloat16_rn(x[2 * w + 1] - __bfloat162float(h1));
-        h[w] = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
-        l[w] = (uint32_t)__bfloat16_as_ushort(l0) | ((uint32_t)__bfloat16_as_ushort(l1) << 16);
-      }
-      const int off = (k16 >> 3) * atom_bytes + r * 128 + (((k16 & 7) ^ (r & 7)) << 4);
-      *reinterpret_cast<uint4*>(hi_tile + off) = make_uint4(h[0], h[1], h[2], h[3]);
-      *reinterpret_cast<uint4*>(lo_tile + off) = make_uint4(l[0], l[1], l[2], l[3]);
-    }
+    for (int w = 0; w < 8; ++w) x[w] = 0.f;
   }
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    const __nv_bfloat16 h0 = __float2bfloat16_rn(x[2 * w]), h1 = __float2bfloat16_rn(x[2 * w + 1]);
+    const __nv_bfloat16 l0 = __float2bfloat16_rn(x[2 * w] - __bfloat162float(h0));
+    const __nv_bfloat16 l1 = __float2bfloat16_rn(x[2 * w + 1] - __bfloat162float(h1));
+    h[w] = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
+    l[w] = (uint32_t)__bfloat16_as_ushort(l0) | ((uint32_t)__bfloat16_as_ushort(l1) << 16);
+  }
+  unsigned char* tile = (isk ? ks : qs) + (bh * T + (row >> 7)) * (size_t)ST::BYTES;
+  const size_t off = ST::offset(row, c16);
+  *reinterpret_cast<uint4*>(tile + off) = make_uint4(h[0], h[1], h[2], h[3]);
+  *reinterpret_cast<uint4*>(tile + ST::HALF + off) = make_uint4(l[0], l[1], l[2], l[3]);
 }
 
+// z = s * qbar kbar^T on the tensor cores (north_star: "tensor cores are used ... in the QK^T of the
+// pooled scores"), the log-size bias and the row softmax, in two passes that recompute the MMA instead
+// of storing logits (the MMA is cheap; the n x n map is written to HBM exactly once):
+//   pass 0 (score_kernel<D, false>): per (row tile, column chunk) the rows' online (max, sum 2^(v - max))
+//          over the chunk's columns -> part[bh][row][chunk];
+//   pass 1 (score_kernel<D, true>):  the row's chunk partials combined in a fixed order, the logits
+//          recomputed and W = 2^(v - m) / l written through a swizzled shared-memory stage as coalesced
+//          row segments.
+// v = (s z + ln|I_j|) log2 e; z = A_hi B_hi^T + A_hi B_lo^T + A_lo B_hi^T from the pre-split tiles of
+// pool_kernel (one bulk copy per operand tile), fp32 accumulation in TMEM.  One CTA per (row tile of 128
+// blocks, chunk of up to 4 column tiles of 128, head); thread = row; the next column tile's MMA runs
+// while the current one's epilogue reads TMEM (two accumulators), and its B tile streams in meanwhile.
 template <int D>
-__global__ void __launch_bounds__(128, 2) score_tc_kernel(const float* __restrict__ qbar, const float* __restrict__ kbar,
-                                                          const float* __restrict__ log_sizes, float* __restrict__ W,
-                                                          float2* __restrict__ part, int n, float scale) {
-  using C = ScoreCfg<D>;
+struct Score2Cfg {
+  using ST = SplitTile<D>;
+  static constexpr int CHUNK = 4;                          // column tiles per CTA
+  static constexpr int OP = ST::BYTES;                     // one operand tile (hi + lo)
+  static constexpr int OFF_A = 0, OFF_B = OP;              // A, then the B ring (2 tiles)
+  static constexpr int STAGE_BYTES = 128 * 128 * 4;        // W staging of one 128 x 128 tile
+  static constexpr bool STAGE_IN_B = OP >= STAGE_BYTES;    // D = 128: reuse the consumed B tile
+  static constexpr int OFF_ST = OFF_B + 2 * OP;            // D = 64: dedicated staging
+  static constexpr int OFF_BAR = OFF_ST + (STAGE_IN_B ? 0 : STAGE_BYTES);   // one stage: written, synced, stored
+  static constexpr int SMEM = OFF_BAR + 64 + 1024;         // + alignment slack
+  static constexpr uint32_t IDESC = idesc_bf16_f32(128, 128, false, false);
+};
+
+template <int D, bool WRITE>
+__global__ void __launch_bounds__(256, 1) score_kernel(const unsigned char* __restrict__ qs,
+                                                       const unsigned char* __restrict__ ks,
+                                                       const float* __restrict__ log_sizes, float* __restrict__ W,
+                                                       float2* __restrict__ part, int n, int T, int NCH,
+                                                       float scale) {
+  using C = Score2Cfg<D>;
+  using ST = SplitTile<D>;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* done = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_BAR + 8);
+  uint64_t* bar_a = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* bar_b = bar_a + 1;      // [2]
+  uint64_t* done = bar_a + 3;       // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_a + 5);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int c0 = blockIdx.x * C::TN, r0 = blockIdx.y * C::TM;
-  const int Tc = gridDim.x;
+  const int rt = blockIdx.x, ch = blockIdx.y;
   const size_t bh = blockIdx.z;
-  const float* Q = qbar + bh * (size_t)n * D;
-  const float* K = kbar + bh * (size_t)n * D;
-  float* Wh = W + bh * (size_t)n * n;
+  const int ct0 = ch * C::CHUNK, nt = min(C::CHUNK, T - ct0);
+  const unsigned char* A = qs + (bh * T + rt) * (size_t)C::OP;
+  const unsigned char* Bt = ks + bh * T * (size_t)C::OP;
   const float L2E = 1.4426950408889634f;
-
+  const float sl2 = scale * L2E;
+  const int row = (warp & 3) * 32 + lane;     // tile row = TMEM lane (warp w reads lane quarter w % 4)
+  const int half = warp >> 2;                 // column half [64 half, +64) of each tile this thread handles
+  const int grow = rt * 128 + row;
+  __shared__ float ls2[C::CHUNK * 128];       // ln|I_j| log2 e of the chunk's columns (-inf past n)
+  for (int e = threadIdx.x; e < C::CHUNK * 128; e += blockDim.x) {
+    const int c = ct0 * 128 + e;
+    ls2[e] = c < n ? log_sizes[c] * L2E : -INFINITY;
+  }
   if (threadIdx.x == 0) {
-    mbar_init(done, 1);
+    mbar_init(bar_a, 1);
+    mbar_init(&bar_b[0], 1);
+    mbar_init(&bar_b[1], 1);
+    mbar_init(&done[0], 1);
+    mbar_init(&done[1], 1);
     fence_mbar_init();
   }
-  if (warp == 0) tmem_alloc<64>(tmem_slot);
-  build_split<D, C::TM>(Q, r0, n, smem + C::OFF_AH, smem + C::OFF_AL, C::A_ATOM, threadIdx.x);
-  build_split<D, C::TN>(K, c0, n, smem + C::OFF_BH, smem + C::OFF_BL, C::B_ATOM, threadIdx.x);
-  fence_async_shared();
+  if (warp == 0) tmem_alloc<256>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  if (threadIdx.x == 0) {
-    const uint32_t ah = smem_u32(smem + C::OFF_AH), al = smem_u32(smem + C::OFF_AL);
-    const uint32_t bhs = smem_u32(smem + C::OFF_BH), bls = smem_u32(smem + C::OFF_BL);
+  // final (m, l) of the row (pass 1): its chunk partials in chunk order
+  float m_row = -INFINITY, l_row = 0.f;
+  if (WRITE && grow < n) {
+    const float2* pr = part + (bh * n + grow) * NCH;
+    for (int c = 0; c < NCH; ++c) m_row = fmaxf(m_row, pr[c].x);
+    for (int c = 0; c < NCH; ++c)
+      if (pr[c].x > -INFINITY) l_row += pr[c].y * ex2(pr[c].x - m_row);
+  }
+  const float inv_l = 1.0f / l_row;
+  auto load_b = [&](int i) {   // thread 0
+    const int s = i & 1;
+    mbar_arrive_expect_tx(&bar_b[s], C::OP);
+    bulk_load(smem + C::OFF_B + s * C::OP, Bt + (size_t)(ct0 + i) * C::OP, C::OP, &bar_b[s]);
+  };
+  auto issue = [&](int i) {   // thread 0: z tile i into accumulator i & 1
+    const int s = i & 1;
+    mbar_wait(&bar_b[s], (i >> 1) & 1);
+    tc_fence_after();
+    const uint32_t ah = smem_u32(smem + C::OFF_A), al = ah + ST::HALF;
+    const uint32_t bhs = smem_u32(smem + C::OFF_B + s * C::OP), bls = bhs + ST::HALF;
 #pragma unroll
     for (int kk = 0; kk < D / 16; ++kk) {
-      const uint32_t ko = (kk % 4) * 32;
-      const uint64_t dah = smem_desc_sw128(ah + (kk / 4) * C::A_ATOM + ko, 16, 1024);
-      const uint64_t dal = smem_desc_sw128(al + (kk / 4) * C::A_ATOM + ko, 16, 1024);
-      const uint64_t dbh = smem_desc_sw128(bhs + (kk / 4) * C::B_ATOM + ko, 16, 1024);
-      const uint64_t dbl = smem_desc_sw128(bls + (kk / 4) * C::B_ATOM + ko, 16, 1024);
-      mma_ss(tmem, dah, dbh, C::IDESC, kk > 0 ? 1u : 0u);
-      mma_ss(tmem, dah, dbl, C::IDESC, 1u);
-      mma_ss(tmem, dal, dbh, C::IDESC, 1u);
+      const uint32_t ko = (kk / 4) * ST::ATOM + (kk % 4) * 32;
+      const uint64_t dah = smem_desc_sw128(ah + ko, 16, 1024), dal = smem_desc_sw128(al + ko, 16, 1024);
+      const uint64_t dbh = smem_desc_sw128(bhs + ko, 16, 1024), dbl = smem_desc_sw128(bls + ko, 16, 1024);
+      const uint32_t d = tmem + s * 128;
+      mma_ss(d, dah, dbh, C::IDESC, kk > 0 ? 1u : 0u);
+      mma_ss(d, dah, dbl, C::IDESC, 1u);
+      mma_ss(d, dal, dbh, C::IDESC, 1u);
     }
-    mma_commit(done);
+    mma_commit(&done[s]);
+  };
+  if (threadIdx.x == 0) {
+    mbar_arrive_expect_tx(bar_a, C::OP);
+    bulk_load(smem + C::OFF_A, A, C::OP, bar_a);
+    load_b(0);
+    if (nt > 1) load_b(1);
+    mbar_wait(bar_a, 0);
+    issue(0);
   }
-  // epilogue: thread = tile row (warp w reads TMEM lane quarter w)
-  const int row = warp * 32 + lane;
-  const int gr = r0 + row;
-  mbar_wait(done, 0);
-  tc_fence_after();
-  uint32_t z[64];
-  tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16), *reinterpret_cast<uint32_t(*)[32]>(&z[0]));
-  tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + 32, *reinterpret_cast<uint32_t(*)[32]>(&z[32]));
-  tmem_ld_wait();
-  const int valid = min(C::TN, n - c0);
-  const float scale_l2 = scale * L2E;
-  float mx = -INFINITY;
+  float m_part = -INFINITY, l_part = 0.f;     // pass 0: this row's online (max, sum) over the chunk
+  for (int i = 0; i < nt; ++i) {
+    const int s = i & 1, ct = ct0 + i;
+    if (threadIdx.x == 0 && i + 1 < nt) issue(i + 1);   // next tile's MMA overlaps this epilogue
+    mbar_wait(&done[s], (i >> 1) & 1);
+    tc_fence_after();
+    const int valid = min(128, n - ct * 128);
+    float* stage = reinterpret_cast<float*>(smem + (C::STAGE_IN_B ? C::OFF_B + s * C::OP : C::OFF_ST));
 #pragma unroll
-  for (int e = 0; e < 64; ++e) {
-    const float v = e < valid ? fmaf(__uint_as_float(z[e]), scale_l2, __ldg(log_sizes + c0 + e) * L2E) : -INFINITY;
-    z[e] = __float_as_uint(v);
-    mx = fmaxf(mx, v);
+    for (int k2 = 0; k2 < 2; ++k2) {
+      const int k = half * 2 + k2;            // 32-column group of the tile
+      uint32_t z[32];
+      tmem_ld32(tmem + ((uint32_t)((warp & 3) * 32) << 16) + s * 128 + k * 32, z);
+      tmem_ld_wait();
+      float v[32];
+#pragma unroll
+      for (int e = 0; e < 32; ++e) v[e] = fmaf(__uint_as_float(z[e]), sl2, ls2[i * 128 + k * 32 + e]);
+      if (!WRITE) {
+        float mx = v[0];
+#pragma unroll
+        for (int e = 1; e < 32; ++e) mx = fmaxf(mx, v[e]);
+        const float m_new = fmaxf(m_part, mx);
+        float sum = 0.f;
+#pragma unroll
+        for (int e = 0; e < 32; ++e) sum += ex2(v[e] - m_new);
+        l_part = (m_part > -INFINITY ? l_part * ex2(m_part - m_new) : 0.f) + sum;
+        m_part = m_new;
+      } else {
+        // W row segment into the stage: float4 chunk cq of row r at chunk (cq ^ (r & 31)) (conflict-free
+        // both for this thread-per-row store and the warp-per-row read below)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int cq = k * 8 + u;
+          float4 w4;
+          w4.x = ex2(v[4 * u] - m_row) * inv_l;
+          w4.y = ex2(v[4 * u + 1] - m_row) * inv_l;
+          w4.z = ex2(v[4 * u + 2] - m_row) * inv_l;
+          w4.w = ex2(v[4 * u + 3] - m_row) * inv_l;
+          reinterpret_cast<float4*>(stage)[row * 32 + (cq ^ (row & 31))] = w4;
+        }
+      }
+    }
+    tc_fence_before();
+    __syncthreads();   // TMEM accumulator s read by everyone; stage s complete; B tile s consumed by MMA i
+    if (WRITE) {
+      // warp w writes rows w, w + 4, ...: 128 B per instruction along the row
+      for (int r = warp; r < 128 && rt * 128 + r < n; r += 8) {
+        float* dst = W + (bh * n + rt * 128 + r) * (size_t)n + ct * 128;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int c = k * 32 + lane;
+          if (c < valid) dst[c] = stage[r * 128 + (((c >> 2) ^ (r & 31)) << 2) + (c & 3)];
+        }
+      }
+      __syncthreads();   // stage s (the B tile s when STAGE_IN_B) free again
+    }
+    tc_fence_after();
+    if (threadIdx.x == 0 && i + 2 < nt) load_b(i + 2);
   }
-  float sum = 0.f;
-#pragma unroll
-  for (int e = 0; e < 64; ++e) sum += exp2f(__uint_as_float(z[e]) - mx);
-  if (gr < n) {
-    part[(bh * n + gr) * Tc + blockIdx.x] = make_float2(mx, sum);
-    float* dst = Wh + (size_t)gr * n + c0;
-    if (valid == 64 && (((uintptr_t)dst & 15) == 0)) {
-#pragma unroll
-      for (int e = 0; e < 16; ++e)
-        reinterpret_cast<uint4*>(dst)[e] = make_uint4(z[4 * e], z[4 * e + 1], z[4 * e + 2], z[4 * e + 3]);
-    } else {
-#pragma unroll
-      for (int e = 0; e < 64; ++e)
-        if (e < valid) dst[e] = __uint_as_float(z[e]);
+  if (!WRITE) {   // the two column halves of each row (warps w and w + 4), combined in a fixed order
+    float2* xr = reinterpret_cast<float2*>(ls2);   // reuse: 128 rows x float2 of the upper half
+    __syncthreads();
+    if (half == 1) xr[row] = make_float2(m_part, l_part);
+    __syncthreads();
+    if (half == 0 && grow < n) {
+      const float2 o = xr[row];
+      const float m = fmaxf(m_part, o.x);
+      const float l = (m_part > -INFINITY ? l_part * ex2(m_part - m) : 0.f) + (o.x > -INFINITY ? o.y * ex2(o.x - m) : 0.f);
+      part[(bh * n + grow) * NCH + ch] = make_float2(m, l);
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {
     tc_fence_after();
-    tmem_dealloc<64>(tmem);
+    tmem_dealloc<256>(tmem);
   }
-}
-
-// one warp per (head, row): m = max_t m_t, l = sum_t l_t 2^(m_t - m) in tile order, W = 2^(v - m) / l
-__global__ void __launch_bounds__(256) softmax_norm_kernel(float* __restrict__ W, const float2* __restrict__ part,
-                                                           int n, int Tc, size_t rows) {
-  const size_t gw = (size_t)blockIdx.x * 8 + threadIdx.x / 32;
-  const int lane = threadIdx.x % 32;
-  if (gw >= rows) return;
-  const float2 pt = lane < Tc ? part[gw * Tc + lane] : make_float2(-INFINITY, 0.f);
-  float m = pt.x;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  // fixed-order sum over the tiles (lane order), so the result does not depend on scheduling
-  const float term = (lane < Tc && pt.x > -INFINITY) ? pt.y * exp2f(pt.x - m) : 0.f;
-  float l = 0.f;
-  for (int t = 0; t < Tc; ++t) l += __shfl_sync(0xffffffffu, term, t);
-  const float invl = 1.0f / l;
-  float* p = W + gw * n;
-  for (int c = lane; c < n; c += 32) p[c] = exp2f(p[c] - m) * invl;
 }
 
 }  // namespace
@@ -250,33 +323,33 @@ extern "C" mod_status mod_collect_block_stats(mod_plan P, const void* q, const v
   if (st != MOD_OK) return st;
   MOD_REQUIRE(q && k && stats && ws, MOD_ERR_USAGE, "mod_collect_block_stats: q, k, stats, ws must be non-NULL");
   const int BH = P->L.batch * P->L.heads, n = P->n, D = P->L.head_dim;
-  float* qbar = reinterpret_cast<float*>(static_cast<char*>(ws) + P->ws_qbar);
+  const int T = (n + 127) / 128, NCH = (T + Score2Cfg<128>::CHUNK - 1) / Score2Cfg<128>::CHUNK;
+  float* qbar = reinterpret_cast<float*>(static_cast<char*>(ws) + P->ws_qbar);   // fp32 means [BH, n, D]
   float* kbar = reinterpret_cast<float*>(static_cast<char*>(ws) + P->ws_kbar);
+  unsigned char* qs = static_cast<unsigned char*>(ws) + P->ws_qs;                  // pre-split tiles [BH][T][hi|lo]
+  unsigned char* ks = static_cast<unsigned char*>(ws) + P->ws_ks;
   cudaStream_t s = as_stream(stream);
   const dim3 pg(n, BH, 2);
-  if (D == 128)
-    pool_kernel<128><<<pg, 256, 0, s>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k, qbar, kbar, P->N, n,
-                                        P->L.block);
-  else
-    pool_kernel<64><<<pg, 256, 0, s>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k, qbar, kbar, P->N, n,
-                                       P->L.block);
-  MOD_LAUNCH_CHECK();
-  const int Tc = (n + 63) / 64;   // <= 32 column tiles (n <= kMaxBlocks = 2048)
-  const dim3 sg(Tc, (n + 127) / 128, BH);
-  float2* part = reinterpret_cast<float2*>(static_cast<char*>(ws) + P->ws_part);   // [BH, n, Tc] (free during K1)
-  if (D == 128) {
-    MOD_CUDA(cudaFuncSetAttribute(score_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  ScoreCfg<128>::SMEM));
-    score_tc_kernel<128><<<sg, 128, ScoreCfg<128>::SMEM, s>>>(qbar, kbar, P->d_log_sizes, stats, part, n, P->scale);
-  } else {
-    MOD_CUDA(cudaFuncSetAttribute(score_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  ScoreCfg<64>::SMEM));
-    score_tc_kernel<64><<<sg, 128, ScoreCfg<64>::SMEM, s>>>(qbar, kbar, P->d_log_sizes, stats, part, n, P->scale);
-  }
-  MOD_LAUNCH_CHECK();
-  const size_t rows = (size_t)BH * n;
-  softmax_norm_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(stats, part, n, Tc, rows);
-  MOD_LAUNCH_CHECK();
-  mod_note_launches(3);
+  const dim3 sg(T, NCH, BH);
+  float2* part = reinterpret_cast<float2*>(static_cast<char*>(ws) + P->ws_part);   // [BH, n, NCH] (free during K1)
+  auto run = [&](auto dc) -> mod_status {
+    constexpr int DD = decltype(dc)::value;
+    using C = Score2Cfg<DD>;
+    pool_kernel<DD><<<pg, 256, 0, s>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k, qbar, kbar, P->N, n, P->L.block);
+    MOD_LAUNCH_CHECK();
+    const size_t chunks = 2ull * BH * T * 128 * (DD / 8);
+    split_kernel<DD><<<(unsigned)((chunks + 255) / 256), 256, 0, s>>>(qbar, kbar, qs, ks, n, T, BH);
+    MOD_LAUNCH_CHECK();
+    MOD_CUDA(cudaFuncSetAttribute(score_kernel<DD, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    MOD_CUDA(cudaFuncSetAttribute(score_kernel<DD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    score_kernel<DD, false><<<sg, 256, C::SMEM, s>>>(qs, ks, P->d_log_sizes, stats, part, n, T, NCH, P->scale);
+    MOD_LAUNCH_CHECK();
+    score_kernel<DD, true><<<sg, 256, C::SMEM, s>>>(qs, ks, P->d_log_sizes, stats, part, n, T, NCH, P->scale);
+    MOD_LAUNCH_CHECK();
+    return MOD_OK;
+  };
+  st = D == 128 ? run(std::integral_constant<int, 128>{}) : run(std::integral_constant<int, 64>{});
+  if (st != MOD_OK) return st;
+  mod_note_launches(4);
   return MOD_OK;
 }
