@@ -135,124 +135,145 @@ __global__ void __launch_bounds__(256) split_kernel(const float* __restrict__ qb
 //   pass 1 (score_kernel<D, true>):  the row's chunk partials combined in a fixed order, the logits
 //          recomputed and W = 2^(v - m) / l written through a swizzled shared-memory stage as coalesced
 //          row segments.
-// v = (s z + ln|I_j|) log2 e; z = A_hi B_hi^T + A_hi B_lo^T + A_lo B_hi^T from the pre-split tiles of
-// pool_kernel (one bulk copy per operand tile), fp32 accumulation in TMEM.  One CTA per (row tile of 128
-// blocks, chunk of up to 4 column tiles of 128, head); thread = row; the next column tile's MMA runs
-// while the current one's epilogue reads TMEM (two accumulators), and its B tile streams in meanwhile.
+// v = (s z + ln|I_j|) log2 e; z = A_hi B_hi^T + A_hi B_lo^T + A_lo B_hi^T from the pre-split tiles
+// (fp32 accumulation in TMEM).  One CTA per (128-row tile, chunk of 512 columns, head), warp-specialised:
+// warp 8 (one thread) streams the chunk's 64-column B sub-tiles by bulk copy through a 3-deep ring and
+// issues the MMAs into two TMEM accumulators; warps 0-7 (thread = row, half of a sub-tile's columns) run
+// the epilogue of sub-tile i while the MMA of i+1 and the copies of i+2.. proceed.
 template <int D>
 struct Score2Cfg {
   using ST = SplitTile<D>;
-  static constexpr int CHUNK = 4;                          // column tiles per CTA
-  static constexpr int OP = ST::BYTES;                     // one operand tile (hi + lo)
-  static constexpr int OFF_A = 0, OFF_B = OP;              // A, then the B ring (2 tiles)
-  static constexpr int STAGE_BYTES = 128 * 128 * 4;        // W staging of one 128 x 128 tile
-  static constexpr bool STAGE_IN_B = OP >= STAGE_BYTES;    // D = 128: reuse the consumed B tile
-  static constexpr int OFF_ST = OFF_B + 2 * OP;            // D = 64: dedicated staging
-  static constexpr int OFF_BAR = OFF_ST + (STAGE_IN_B ? 0 : STAGE_BYTES);   // one stage: written, synced, stored
-  static constexpr int SMEM = OFF_BAR + 64 + 1024;         // + alignment slack
-  static constexpr uint32_t IDESC = idesc_bf16_f32(128, 128, false, false);
+  static constexpr int TN = 64;                            // columns per sub-tile (MMA N)
+  static constexpr int CHUNK_COLS = 512;                   // columns per CTA
+  static constexpr int NB = 3;                             // B ring depth
+  static constexpr int OPA = ST::BYTES;                    // A tile (128 rows, hi + lo)
+  static constexpr int SUB = ST::NATOM * 64 * 128;         // one 64-row piece of hi (or lo)
+  static constexpr int OPB = 2 * SUB;                      // B sub-tile (64 rows, hi + lo)
+  static constexpr int STAGE_BYTES = 128 * TN * 4;
+  static constexpr int OFF_A = 0, OFF_B = OPA, OFF_ST = OFF_B + NB * OPB;
+  static constexpr int OFF_BAR = OFF_ST + 2 * STAGE_BYTES;
+  static constexpr int OFF_LS = OFF_BAR + 128;             // ln|I_j| log2 e of the chunk's columns
+  static constexpr int SMEM = OFF_LS + CHUNK_COLS * 4;     // 226 KB at D = 128
+  static constexpr int THREADS = 288;
+  static constexpr uint32_t IDESC = idesc_bf16_f32(128, TN, false, false);
 };
 
 template <int D, bool WRITE>
-__global__ void __launch_bounds__(256, 1) score_kernel(const unsigned char* __restrict__ qs,
-                                                       const unsigned char* __restrict__ ks,
-                                                       const float* __restrict__ log_sizes, float* __restrict__ W,
-                                                       float2* __restrict__ part, int n, int T, int NCH,
-                                                       float scale) {
+__global__ void __launch_bounds__(Score2Cfg<D>::THREADS, 1) score_kernel(
+    const unsigned char* __restrict__ qs, const unsigned char* __restrict__ ks, const float* __restrict__ log_sizes,
+    float* __restrict__ W, float2* __restrict__ part, int n, int T, int NCH, float scale) {
   using C = Score2Cfg<D>;
   using ST = SplitTile<D>;
-  extern __shared__ unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bar_a = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
-  uint64_t* bar_b = bar_a + 1;      // [2]
-  uint64_t* done = bar_a + 3;       // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_a + 5);
+  extern __shared__ __align__(1024) unsigned char smem[];
+  if (threadIdx.x == 0 && (smem_u32(smem) & 1023u) != 0) __trap();   // SWIZZLE_128B operands need 1024B alignment
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* b_full = a_full + 1;          // [NB]
+  uint64_t* b_empty = b_full + C::NB;     // [NB]  (MMA commit: the sub-tile's MMAs have read the buffer)
+  uint64_t* acc_full = b_empty + C::NB;   // [2]
+  uint64_t* acc_empty = acc_full + 2;     // [2]   (8 epilogue warps have read the accumulator)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int rt = blockIdx.x, ch = blockIdx.y;
   const size_t bh = blockIdx.z;
-  const int ct0 = ch * C::CHUNK, nt = min(C::CHUNK, T - ct0);
-  const unsigned char* A = qs + (bh * T + rt) * (size_t)C::OP;
-  const unsigned char* Bt = ks + bh * T * (size_t)C::OP;
+  const int c0 = ch * C::CHUNK_COLS;
+  const int nt = min(C::CHUNK_COLS / C::TN, (n - c0 + C::TN - 1) / C::TN);   // sub-tiles of this chunk
   const float L2E = 1.4426950408889634f;
   const float sl2 = scale * L2E;
-  const int row = (warp & 3) * 32 + lane;     // tile row = TMEM lane (warp w reads lane quarter w % 4)
-  const int half = warp >> 2;                 // column half [64 half, +64) of each tile this thread handles
-  const int grow = rt * 128 + row;
-  __shared__ float ls2[C::CHUNK * 128];       // ln|I_j| log2 e of the chunk's columns (-inf past n)
-  for (int e = threadIdx.x; e < C::CHUNK * 128; e += blockDim.x) {
-    const int c = ct0 * 128 + e;
+  float* ls2 = reinterpret_cast<float*>(smem + C::OFF_LS);   // -inf past n
+  for (int e = threadIdx.x; e < C::CHUNK_COLS; e += blockDim.x) {
+    const int c = c0 + e;
     ls2[e] = c < n ? log_sizes[c] * L2E : -INFINITY;
   }
   if (threadIdx.x == 0) {
-    mbar_init(bar_a, 1);
-    mbar_init(&bar_b[0], 1);
-    mbar_init(&bar_b[1], 1);
-    mbar_init(&done[0], 1);
-    mbar_init(&done[1], 1);
+    mbar_init(a_full, 1);
+    for (int i = 0; i < C::NB; ++i) {
+      mbar_init(&b_full[i], 1);
+      mbar_init(&b_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 8);
+    }
     fence_mbar_init();
   }
-  if (warp == 0) tmem_alloc<256>(tmem_slot);
+  if (warp == 8) tmem_alloc<128>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // final (m, l) of the row (pass 1): its chunk partials in chunk order
-  float m_row = -INFINITY, l_row = 0.f;
-  if (WRITE && grow < n) {
-    const float2* pr = part + (bh * n + grow) * NCH;
-    for (int c = 0; c < NCH; ++c) m_row = fmaxf(m_row, pr[c].x);
-    for (int c = 0; c < NCH; ++c)
-      if (pr[c].x > -INFINITY) l_row += pr[c].y * ex2(pr[c].x - m_row);
-  }
-  const float inv_l = 1.0f / l_row;
-  auto load_b = [&](int i) {   // thread 0
-    const int s = i & 1;
-    mbar_arrive_expect_tx(&bar_b[s], C::OP);
-    bulk_load(smem + C::OFF_B + s * C::OP, Bt + (size_t)(ct0 + i) * C::OP, C::OP, &bar_b[s]);
-  };
-  auto issue = [&](int i) {   // thread 0: z tile i into accumulator i & 1
-    const int s = i & 1;
-    mbar_wait(&bar_b[s], (i >> 1) & 1);
-    tc_fence_after();
-    const uint32_t ah = smem_u32(smem + C::OFF_A), al = ah + ST::HALF;
-    const uint32_t bhs = smem_u32(smem + C::OFF_B + s * C::OP), bls = bhs + ST::HALF;
+
+  if (warp == 8) {
+    // ------------------------------------------------------------ bulk copies + MMA issue (one thread)
+    if (lane == 0) {
+      const unsigned char* A = qs + (bh * T + rt) * (size_t)C::OPA;
+      auto load_b = [&](int i) {
+        const int sb = i % C::NB;
+        const int col = c0 + i * C::TN;                       // first column: rows of k-bar tile col / 128
+        const unsigned char* tile = ks + (bh * T + col / 128) * (size_t)ST::BYTES + (col % 128) * 128;
+        unsigned char* dst = smem + C::OFF_B + sb * C::OPB;
+        mbar_arrive_expect_tx(&b_full[sb], C::OPB);
 #pragma unroll
-    for (int kk = 0; kk < D / 16; ++kk) {
-      const uint32_t ko = (kk / 4) * ST::ATOM + (kk % 4) * 32;
-      const uint64_t dah = smem_desc_sw128(ah + ko, 16, 1024), dal = smem_desc_sw128(al + ko, 16, 1024);
-      const uint64_t dbh = smem_desc_sw128(bhs + ko, 16, 1024), dbl = smem_desc_sw128(bls + ko, 16, 1024);
-      const uint32_t d = tmem + s * 128;
-      mma_ss(d, dah, dbh, C::IDESC, kk > 0 ? 1u : 0u);
-      mma_ss(d, dah, dbl, C::IDESC, 1u);
-      mma_ss(d, dal, dbh, C::IDESC, 1u);
+        for (int hl = 0; hl < 2; ++hl)
+#pragma unroll
+          for (int a = 0; a < ST::NATOM; ++a)
+            bulk_load(dst + hl * C::SUB + a * 64 * 128, tile + hl * ST::HALF + a * ST::ATOM, 64 * 128, &b_full[sb]);
+      };
+      mbar_arrive_expect_tx(a_full, C::OPA);
+      bulk_load(smem + C::OFF_A, A, C::OPA, a_full);
+      for (int i = 0; i < C::NB && i < nt; ++i) load_b(i);
+      mbar_wait(a_full, 0);
+      const uint32_t ah = smem_u32(smem + C::OFF_A), al = ah + ST::HALF;
+      for (int i = 0; i < nt; ++i) {
+        const int sb = i % C::NB, s = i & 1;
+        mbar_wait(&b_full[sb], (i / C::NB) & 1);
+        if (i >= 2) mbar_wait(&acc_empty[s], ((i >> 1) - 1) & 1);   // epilogue of sub-tile i-2 read acc s
+        tc_fence_after();
+        const uint32_t bhs = smem_u32(smem + C::OFF_B + sb * C::OPB), bls = bhs + C::SUB;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t ka = (kk / 4) * ST::ATOM + (kk % 4) * 32, kb = (kk / 4) * (64 * 128) + (kk % 4) * 32;
+          const uint64_t dah = smem_desc_sw128(ah + ka, 16, 1024), dal = smem_desc_sw128(al + ka, 16, 1024);
+          const uint64_t dbh = smem_desc_sw128(bhs + kb, 16, 1024), dbl = smem_desc_sw128(bls + kb, 16, 1024);
+          const uint32_t d = tmem + s * C::TN;
+          mma_ss(d, dah, dbh, C::IDESC, kk > 0 ? 1u : 0u);
+          mma_ss(d, dah, dbl, C::IDESC, 1u);
+          mma_ss(d, dal, dbh, C::IDESC, 1u);
+        }
+        mma_commit(&acc_full[s]);
+        mma_commit(&b_empty[sb]);
+        if (i >= 1 && i - 1 + C::NB < nt) {   // refill the buffer sub-tile i-1 used (its MMAs precede these)
+          mbar_wait(&b_empty[(i - 1) % C::NB], ((i - 1) / C::NB) & 1);
+          load_b(i - 1 + C::NB);
+        }
+      }
     }
-    mma_commit(&done[s]);
-  };
-  if (threadIdx.x == 0) {
-    mbar_arrive_expect_tx(bar_a, C::OP);
-    bulk_load(smem + C::OFF_A, A, C::OP, bar_a);
-    load_b(0);
-    if (nt > 1) load_b(1);
-    mbar_wait(bar_a, 0);
-    issue(0);
-  }
-  float m_part = -INFINITY, l_part = 0.f;     // pass 0: this row's online (max, sum) over the chunk
-  for (int i = 0; i < nt; ++i) {
-    const int s = i & 1, ct = ct0 + i;
-    if (threadIdx.x == 0 && i + 1 < nt) issue(i + 1);   // next tile's MMA overlaps this epilogue
-    mbar_wait(&done[s], (i >> 1) & 1);
-    tc_fence_after();
-    const int valid = min(128, n - ct * 128);
-    float* stage = reinterpret_cast<float*>(smem + (C::STAGE_IN_B ? C::OFF_B + s * C::OP : C::OFF_ST));
-#pragma unroll
-    for (int k2 = 0; k2 < 2; ++k2) {
-      const int k = half * 2 + k2;            // 32-column group of the tile
+  } else {
+    // ------------------------------------------------------------ epilogue: thread = (row, column half)
+    const int row = (warp & 3) * 32 + lane;
+    const int half = warp >> 2;             // columns [32 half, +32) of each 64-column sub-tile
+    const int grow = rt * 128 + row;
+    float m_row = -INFINITY, l_row = 0.f;
+    if (WRITE && grow < n) {   // final (m, l) of the row: its chunk partials in chunk order
+      const float2* pr = part + (bh * n + grow) * NCH;
+      for (int c = 0; c < NCH; ++c) m_row = fmaxf(m_row, pr[c].x);
+      for (int c = 0; c < NCH; ++c)
+        if (pr[c].x > -INFINITY) l_row += pr[c].y * ex2(pr[c].x - m_row);
+    }
+    const float inv_l = 1.0f / l_row;
+    float m_part = -INFINITY, l_part = 0.f;
+    for (int i = 0; i < nt; ++i) {
+      const int s = i & 1;
+      mbar_wait(&acc_full[s], (i >> 1) & 1);
+      tc_fence_after();
       uint32_t z[32];
-      tmem_ld32(tmem + ((uint32_t)((warp & 3) * 32) << 16) + s * 128 + k * 32, z);
+      tmem_ld32(tmem + ((uint32_t)((warp & 3) * 32) << 16) + s * C::TN + half * 32, z);
       tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[s]);
       float v[32];
 #pragma unroll
-      for (int e = 0; e < 32; ++e) v[e] = fmaf(__uint_as_float(z[e]), sl2, ls2[i * 128 + k * 32 + e]);
+      for (int e = 0; e < 32; ++e) v[e] = fmaf(__uint_as_float(z[e]), sl2, ls2[i * C::TN + half * 32 + e]);
       if (!WRITE) {
         float mx = v[0];
 #pragma unroll
@@ -264,54 +285,47 @@ __global__ void __launch_bounds__(256, 1) score_kernel(const unsigned char* __re
         l_part = (m_part > -INFINITY ? l_part * ex2(m_part - m_new) : 0.f) + sum;
         m_part = m_new;
       } else {
-        // W row segment into the stage: float4 chunk cq of row r at chunk (cq ^ (r & 31)) (conflict-free
-        // both for this thread-per-row store and the warp-per-row read below)
+        float* stage = reinterpret_cast<float*>(smem + C::OFF_ST + s * C::STAGE_BYTES);
+        // float4 chunk cq (0..15) of row r at chunk (cq ^ (r & 15)): spread banks for both access orders
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          const int cq = k * 8 + u;
+          const int cq = half * 8 + u;
           float4 w4;
           w4.x = ex2(v[4 * u] - m_row) * inv_l;
           w4.y = ex2(v[4 * u + 1] - m_row) * inv_l;
           w4.z = ex2(v[4 * u + 2] - m_row) * inv_l;
           w4.w = ex2(v[4 * u + 3] - m_row) * inv_l;
-          reinterpret_cast<float4*>(stage)[row * 32 + (cq ^ (row & 31))] = w4;
+          reinterpret_cast<float4*>(stage)[row * 16 + (cq ^ (row & 15))] = w4;
         }
-      }
-    }
-    tc_fence_before();
-    __syncthreads();   // TMEM accumulator s read by everyone; stage s complete; B tile s consumed by MMA i
-    if (WRITE) {
-      // warp w writes rows w, w + 4, ...: 128 B per instruction along the row
-      for (int r = warp; r < 128 && rt * 128 + r < n; r += 8) {
-        float* dst = W + (bh * n + rt * 128 + r) * (size_t)n + ct * 128;
+        named_bar_sync(1, 256);
+        const int cb = c0 + i * C::TN, valid = min(C::TN, n - cb);
+        for (int r = warp; r < 128 && rt * 128 + r < n; r += 8) {
+          float* dst = W + (bh * n + rt * 128 + r) * (size_t)n + cb;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int c = k * 32 + lane;
-          if (c < valid) dst[c] = stage[r * 128 + (((c >> 2) ^ (r & 31)) << 2) + (c & 3)];
+          for (int k = 0; k < 2; ++k) {
+            const int c = k * 32 + lane;
+            if (c < valid) dst[c] = stage[r * 64 + (((c >> 2) ^ (r & 15)) << 2) + (c & 3)];
+          }
         }
       }
-      __syncthreads();   // stage s (the B tile s when STAGE_IN_B) free again
     }
-    tc_fence_after();
-    if (threadIdx.x == 0 && i + 2 < nt) load_b(i + 2);
-  }
-  if (!WRITE) {   // the two column halves of each row (warps w and w + 4), combined in a fixed order
-    float2* xr = reinterpret_cast<float2*>(ls2);   // reuse: 128 rows x float2 of the upper half
-    __syncthreads();
-    if (half == 1) xr[row] = make_float2(m_part, l_part);
-    __syncthreads();
-    if (half == 0 && grow < n) {
-      const float2 o = xr[row];
-      const float m = fmaxf(m_part, o.x);
-      const float l = (m_part > -INFINITY ? l_part * ex2(m_part - m) : 0.f) + (o.x > -INFINITY ? o.y * ex2(o.x - m) : 0.f);
-      part[(bh * n + grow) * NCH + ch] = make_float2(m, l);
+    if (!WRITE) {   // the two column halves of each row (warps w and w + 4), combined in a fixed order
+      float2* xr = reinterpret_cast<float2*>(smem + C::OFF_ST);
+      if (half == 1) xr[row] = make_float2(m_part, l_part);
+      named_bar_sync(1, 256);
+      if (half == 0 && grow < n) {
+        const float2 o = xr[row];
+        const float m = fmaxf(m_part, o.x);
+        const float l = (m_part > -INFINITY ? l_part * ex2(m_part - m) : 0.f) + (o.x > -INFINITY ? o.y * ex2(o.x - m) : 0.f);
+        part[(bh * n + grow) * NCH + ch] = make_float2(m, l);
+      }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) {
+  if (warp == 8) {
     tc_fence_after();
-    tmem_dealloc<256>(tmem);
+    tmem_dealloc<128>(tmem);
   }
 }
 
@@ -323,7 +337,7 @@ extern "C" mod_status mod_collect_block_stats(mod_plan P, const void* q, const v
   if (st != MOD_OK) return st;
   MOD_REQUIRE(q && k && stats && ws, MOD_ERR_USAGE, "mod_collect_block_stats: q, k, stats, ws must be non-NULL");
   const int BH = P->L.batch * P->L.heads, n = P->n, D = P->L.head_dim;
-  const int T = (n + 127) / 128, NCH = (T + Score2Cfg<128>::CHUNK - 1) / Score2Cfg<128>::CHUNK;
+  const int T = (n + 127) / 128, NCH = (n + Score2Cfg<128>::CHUNK_COLS - 1) / Score2Cfg<128>::CHUNK_COLS;
   float* qbar = reinterpret_cast<float*>(static_cast<char*>(ws) + P->ws_qbar);   // fp32 means [BH, n, D]
   float* kbar = reinterpret_cast<float*>(static_cast<char*>(ws) + P->ws_kbar);
   unsigned char* qs = static_cast<unsigned char*>(ws) + P->ws_qs;                  // pre-split tiles [BH][T][hi|lo]
@@ -342,9 +356,9 @@ extern "C" mod_status mod_collect_block_stats(mod_plan P, const void* q, const v
     MOD_LAUNCH_CHECK();
     MOD_CUDA(cudaFuncSetAttribute(score_kernel<DD, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     MOD_CUDA(cudaFuncSetAttribute(score_kernel<DD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    score_kernel<DD, false><<<sg, 256, C::SMEM, s>>>(qs, ks, P->d_log_sizes, stats, part, n, T, NCH, P->scale);
+    score_kernel<DD, false><<<sg, C::THREADS, C::SMEM, s>>>(qs, ks, P->d_log_sizes, stats, part, n, T, NCH, P->scale);
     MOD_LAUNCH_CHECK();
-    score_kernel<DD, true><<<sg, 256, C::SMEM, s>>>(qs, ks, P->d_log_sizes, stats, part, n, T, NCH, P->scale);
+    score_kernel<DD, true><<<sg, C::THREADS, C::SMEM, s>>>(qs, ks, P->d_log_sizes, stats, part, n, T, NCH, P->scale);
     MOD_LAUNCH_CHECK();
     return MOD_OK;
   };
