@@ -111,6 +111,7 @@ __global__ void linearity_kernel(const double* __restrict__ xp, const double* __
 
 extern "C" mod_status mod_map_rel_error(mod_plan P, const float* a, const float* b, double* out, void* ws,
                                         void* stream) {
+  MOD_NVTX("mod_map_rel_error");
   mod_status st = mod_validate_plan(P);
   if (st != MOD_OK) return st;
   MOD_REQUIRE(a && b && out && ws, MOD_ERR_USAGE, "mod_map_rel_error: a, b, out, ws must be non-NULL");
@@ -133,6 +134,7 @@ extern "C" mod_status mod_map_rel_error(mod_plan P, const float* a, const float*
 extern "C" mod_status mod_linearity_nre(mod_plan P, const double* x_prev, const double* x_curr, int32_t t_prev,
                                         int32_t t_curr, const double* x_traj, const int32_t* t_steps, int32_t S,
                                         double* out, void* stream) {
+  MOD_NVTX("mod_linearity_nre");
   mod_status st = mod_validate_plan(P);
   if (st != MOD_OK) return st;
   MOD_REQUIRE(x_prev && x_curr && x_traj && t_steps && out, MOD_ERR_USAGE,

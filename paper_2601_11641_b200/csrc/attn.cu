@@ -1511,6 +1511,7 @@ extern "C" const char* mod_attn_kernel_name(mod_plan P) {
 extern "C" mod_status mod_block_sparse_attn_fwd(mod_plan P, const void* q, const void* k, const void* v,
                                                 const int32_t* row_ptr, const int32_t* col_idx, void* o, float* lse,
                                                 void* ws, void* stream) {
+  MOD_NVTX("mod_block_sparse_attn_fwd");
   (void)ws;
   mod_status st = mod_validate_plan(P);
   if (st != MOD_OK) return st;

@@ -328,6 +328,7 @@ mod_status make_map_u8(CUtensorMap* m, const void* base, int inner, int rows, in
 extern "C" mod_status mod_block_sparse_attn_fwd_q8(mod_plan P, const void* qbuf, const int32_t* row_ptr,
                                                    const int32_t* col_idx, void* o, float* lse, void* ws,
                                                    void* stream) {
+  MOD_NVTX("mod_block_sparse_attn_fwd_q8");
   (void)ws;
   mod_status st = mod_validate_plan(P);
   if (st != MOD_OK) return st;

@@ -8,6 +8,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "moddit.h"
 
 // ------------------------------------------------------------------------------------------------
@@ -70,6 +72,14 @@ struct mod_plan_s {
 mod_status mod_validate_plan(mod_plan plan);
 
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// NVTX range around every C-ABI entry point (host side: it brackets the enqueue of the call's launches),
+// so that profiler timelines attribute the kernels to mod_* calls; free when no tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+#define MOD_NVTX(name) NvtxRange mod_nvtx_range_(name)
 
 constexpr int kProjRows = 32;    // max rows per projection tile (fit / update)
 constexpr int kProjSmemFloats = 28672;   // shared-memory map tile of the projection (112 KB)

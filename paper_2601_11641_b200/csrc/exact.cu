@@ -214,6 +214,7 @@ mod_status launch_ex(mod_plan P, const void* q, const void* k, const float* lse,
 extern "C" mod_status mod_collect_exact_sparsity(mod_plan P, const void* q, const void* k, const float* lse,
                                                  const int32_t* row_ptr, const int32_t* col_idx, float eta,
                                                  float* stats, void* ws, void* stream) {
+  MOD_NVTX("mod_collect_exact_sparsity");
   (void)ws;
   mod_status st = mod_validate_plan(P);
   if (st != MOD_OK) return st;

@@ -386,6 +386,7 @@ mod_status fit_from_map(mod_plan P, const float* U, double* X, void* ws, cudaStr
 }  // namespace
 
 extern "C" mod_status mod_fit_mixture(mod_plan P, const float* stats, double* x, float* nae, void* ws, void* stream) {
+  MOD_NVTX("mod_fit_mixture");
   mod_status st = mod_validate_plan(P);
   if (st != MOD_OK) return st;
   MOD_REQUIRE(stats && x && ws, MOD_ERR_USAGE, "mod_fit_mixture: stats, x, ws must be non-NULL");
@@ -408,6 +409,7 @@ extern "C" mod_status mod_fit_mixture(mod_plan P, const float* stats, double* x,
 }
 
 extern "C" mod_status mod_keep_frames(mod_plan P, const double* x_a, const double* x_b, uint8_t* keep, void* stream) {
+  MOD_NVTX("mod_keep_frames");
   mod_status st = mod_validate_plan(P);
   if (st != MOD_OK) return st;
   MOD_REQUIRE(x_a && x_b && keep, MOD_ERR_USAGE, "mod_keep_frames: x_a, x_b, keep must be non-NULL");
@@ -422,6 +424,7 @@ extern "C" mod_status mod_keep_frames(mod_plan P, const double* x_a, const doubl
 extern "C" mod_status mod_update_online_mask(mod_plan P, const float* stats_fresh, const int32_t* row_ptr,
                                              const int32_t* col_idx, float* stats_hist, double* x_prev,
                                              double* x_curr, void* ws, void* stream) {
+  MOD_NVTX("mod_update_online_mask");
   mod_status st = mod_validate_plan(P);
   if (st != MOD_OK) return st;
   MOD_REQUIRE(stats_fresh && row_ptr && col_idx && stats_hist && x_prev && x_curr && ws, MOD_ERR_USAGE,

@@ -317,6 +317,7 @@ static std::vector<std::vector<double>> null_space(int n, const std::vector<int>
 static size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 extern "C" mod_status mod_plan_create(const mod_layout* layout, const mod_config* cfg, int device, mod_plan* out) {
+  MOD_NVTX("mod_plan_create");
   MOD_REQUIRE(layout && cfg && out, MOD_ERR_USAGE, "mod_plan_create: layout, cfg and out must be non-NULL");
   const auto t_start = std::chrono::steady_clock::now();
   *out = nullptr;
@@ -605,12 +606,14 @@ extern "C" int32_t mod_plan_gram_inverse_ld(mod_plan P) { return P ? P->ginv_ld 
 extern "C" int32_t mod_plan_solver(mod_plan P) { return P ? P->solver : -1; }
 extern "C" double mod_plan_create_ms(mod_plan P) { return P ? P->create_ms : -1.0; }
 extern "C" mod_status mod_plan_diagnostics(mod_plan P, double* min_pivot, int32_t* null_dim) {
+  MOD_NVTX("mod_plan_diagnostics");
   MOD_REQUIRE(P, MOD_ERR_USAGE, "mod_plan_diagnostics: NULL plan");
   if (min_pivot) *min_pivot = P->min_pivot;
   if (null_dim) *null_dim = P->null_dim;
   return MOD_OK;
 }
 extern "C" mod_status mod_plan_frame_blocks(mod_plan P, int32_t* a_b) {
+  MOD_NVTX("mod_plan_frame_blocks");
   MOD_REQUIRE(P && a_b, MOD_ERR_USAGE, "mod_plan_frame_blocks: NULL argument");
   for (int i = 0; i < 2 * P->F; ++i) a_b[i] = P->frame_ab[i];
   return MOD_OK;

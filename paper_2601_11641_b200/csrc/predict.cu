@@ -367,6 +367,7 @@ extern "C" mod_status mod_predict_block_mask(mod_plan P, const double* x_prev, c
                                              int32_t t_curr, int32_t t, const uint8_t* keep,
                                              const mod_selection* sel, int32_t* row_ptr, int32_t* col_idx,
                                              void* ws, void* stream) {
+  MOD_NVTX("mod_predict_block_mask");
   mod_status st = mod_validate_plan(P);
   if (st != MOD_OK) return st;
   MOD_REQUIRE(x_prev && x_curr && row_ptr && col_idx && ws, MOD_ERR_USAGE,
@@ -415,6 +416,7 @@ extern "C" mod_status mod_predict_block_mask(mod_plan P, const double* x_prev, c
 }
 
 extern "C" mod_status mod_fill_dense_mask(mod_plan P, int32_t* row_ptr, int32_t* col_idx, void* stream) {
+  MOD_NVTX("mod_fill_dense_mask");
   mod_status st = mod_validate_plan(P);
   if (st != MOD_OK) return st;
   MOD_REQUIRE(row_ptr && col_idx, MOD_ERR_USAGE, "mod_fill_dense_mask: NULL argument");

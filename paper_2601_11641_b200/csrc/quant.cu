@@ -196,6 +196,7 @@ extern "C" size_t mod_quant_buffer_bytes(mod_plan P) {
 }
 
 extern "C" mod_status mod_quant_buffer_layout(mod_plan P, size_t* offsets) {
+  MOD_NVTX("mod_quant_buffer_layout");
   mod_status st = mod_validate_plan(P);
   if (st != MOD_OK) return st;
   if ((st = check_quant_plan(P)) != MOD_OK) return st;
@@ -208,6 +209,7 @@ extern "C" mod_status mod_quant_buffer_layout(mod_plan P, size_t* offsets) {
 
 extern "C" mod_status mod_quantize_qkv(mod_plan P, const void* q, const void* k, const void* v, void* qbuf,
                                        void* stream) {
+  MOD_NVTX("mod_quantize_qkv");
   mod_status st = mod_validate_plan(P);
   if (st != MOD_OK) return st;
   if ((st = check_quant_plan(P)) != MOD_OK) return st;

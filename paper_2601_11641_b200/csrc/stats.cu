@@ -333,6 +333,7 @@ __global__ void __launch_bounds__(Score2Cfg<D>::THREADS, 1) score_kernel(
 
 extern "C" mod_status mod_collect_block_stats(mod_plan P, const void* q, const void* k, float* stats, void* ws,
                                               void* stream) {
+  MOD_NVTX("mod_collect_block_stats");
   mod_status st = mod_validate_plan(P);
   if (st != MOD_OK) return st;
   MOD_REQUIRE(q && k && stats && ws, MOD_ERR_USAGE, "mod_collect_block_stats: q, k, stats, ws must be non-NULL");

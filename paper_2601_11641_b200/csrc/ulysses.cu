@@ -123,23 +123,27 @@ mod_status launch(const void* src, void* dst, int B, int Ns, int Hp, int D, int 
 
 extern "C" mod_status mod_ulysses_seq_pack(const void* x_seq, void* send, int32_t B, int32_t Ns, int32_t H,
                                            int32_t D, int32_t P, void* stream) {
+  MOD_NVTX("mod_ulysses_seq_pack");
   MOD_REQUIRE(P >= 1 && H % P == 0, MOD_ERR_INPUT, "mod_ulysses_seq_pack: heads=%d not divisible by P=%d", H, P);
   return launch<SEQ_PACK>(x_seq, send, B, Ns, H / P, D, P, stream);
 }
 
 extern "C" mod_status mod_ulysses_seq_unpack(const void* recv, void* x_head, int32_t B, int32_t Ns, int32_t Hp,
                                              int32_t D, int32_t P, void* stream) {
+  MOD_NVTX("mod_ulysses_seq_unpack");
   return launch<SEQ_UNPACK>(recv, x_head, B, Ns, Hp, D, P, stream);
 }
 
 extern "C" mod_status mod_ulysses_head_pack(const void* x_head, void* send, int32_t B, int32_t N, int32_t Hp,
                                             int32_t D, int32_t P, void* stream) {
+  MOD_NVTX("mod_ulysses_head_pack");
   MOD_REQUIRE(P >= 1 && N % P == 0, MOD_ERR_INPUT, "mod_ulysses_head_pack: tokens=%d not divisible by P=%d", N, P);
   return launch<HEAD_PACK>(x_head, send, B, N / P, Hp, D, P, stream);
 }
 
 extern "C" mod_status mod_ulysses_head_unpack(const void* recv, void* x_seq, int32_t B, int32_t Ns, int32_t Hp,
                                               int32_t D, int32_t P, void* stream) {
+  MOD_NVTX("mod_ulysses_head_unpack");
   return launch<HEAD_UNPACK>(recv, x_seq, B, Ns, Hp, D, P, stream);
 }
 
@@ -147,6 +151,7 @@ extern "C" mod_status mod_ulysses_head_unpack(const void* recv, void* x_seq, int
 // unpack into heads [h0, h0 + P*Hp) of an H-head x_seq.
 extern "C" mod_status mod_ulysses_seq_pack_heads(const void* x_seq, void* send, int32_t B, int32_t Ns, int32_t H,
                                                  int32_t h0, int32_t Hc, int32_t D, int32_t P, void* stream) {
+  MOD_NVTX("mod_ulysses_seq_pack_heads");
   MOD_REQUIRE(P >= 1 && Hc >= 1 && Hc % P == 0, MOD_ERR_INPUT,
               "mod_ulysses_seq_pack_heads: chunk of %d heads not divisible by P=%d", Hc, P);
   return launch<SEQ_PACK>(x_seq, send, B, Ns, Hc / P, D, P, stream, H, h0);
@@ -154,5 +159,6 @@ extern "C" mod_status mod_ulysses_seq_pack_heads(const void* x_seq, void* send, 
 
 extern "C" mod_status mod_ulysses_head_unpack_heads(const void* recv, void* x_seq, int32_t B, int32_t Ns, int32_t Hp,
                                                     int32_t D, int32_t P, int32_t H, int32_t h0, void* stream) {
+  MOD_NVTX("mod_ulysses_head_unpack_heads");
   return launch<HEAD_UNPACK>(recv, x_seq, B, Ns, Hp, D, P, stream, H, h0);
 }
