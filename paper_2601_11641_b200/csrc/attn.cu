@@ -364,6 +364,9 @@ __global__ void __launch_bounds__(320, 1)
 #ifndef K4_WAIT
 #define K4_WAIT mbar_wait_sleep   // producer / MMA-issuer waits (the softmax warps poll)
 #endif
+#ifndef K4_SWAIT
+#define K4_SWAIT mbar_wait        // the softmax warps' wait for S (try_wait loop)
+#endif
 template <int D, int BN>
 struct Attn1Cfg {
   static constexpr int BM = 128;
@@ -631,7 +634,7 @@ __global__ void __launch_bounds__(Attn1Cfg<D, BN>::THREADS, 1)
     const int q_rows = min(block, N - q_row0);
     float m_run = -INFINITY, l_run = 0.f;   // reference max (log2 units, scaled) / this half-row's sum
     const bool tr = lane == 0;
-    const int trole = warp - 1;   // trace role of this softmax warp (1..)
+    [[maybe_unused]] const int trole = warp - 1;   // trace role of this softmax warp (1..)
     int col_next = L > 0 ? cols[0] : 0;   // column index of the next block, loaded one block ahead
 #pragma unroll 1
     for (int j = 0; j < L; ++j) {
@@ -639,7 +642,7 @@ __global__ void __launch_bounds__(Attn1Cfg<D, BN>::THREADS, 1)
       const int col = col_next;
       if (j + 1 < L) col_next = cols[j + 1];
       if (tr) K4T(trole, 0, j);
-      mbar_wait(&s_full[b], (j / NS) & 1);
+      K4_SWAIT(&s_full[b], (j / NS) & 1);
       if (tr) K4T(trole, 1, j);
       tc_fence_after();
       uint32_t sr[COLS];
@@ -953,7 +956,7 @@ __global__ void __launch_bounds__(WideCfg<D, BN>::THREADS, 1)
       const int b = j % NS;
       const int col = col_next;
       if (j + 1 < L) col_next = cols[j + 1];
-      mbar_wait(&s_full[b], (j / NS) & 1);
+      K4_SWAIT(&s_full[b], (j / NS) & 1);
       tc_fence_after();
       uint32_t sr[COLS];
       tmem_ld_rows<COLS, COLS>(tmem + lane_off + b * BN + c * KH, sr);   // keys c*KH + colq*COLS + [0, COLS)
