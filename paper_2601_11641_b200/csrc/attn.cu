@@ -367,6 +367,28 @@ __global__ void __launch_bounds__(320, 1)
 #ifndef K4_SWAIT
 #define K4_SWAIT mbar_wait        // the softmax warps' wait for S (try_wait loop)
 #endif
+// MMA issue form.  K4_LANE0_ISSUE = 1: one lane of the issuing warp runs the issue loop (the other lanes
+// leave it).  0: the whole warp runs it converged and elect.sync picks the issuing lane per MMA.  Measured
+// (scripts/micro/interference_probe.cu): a converged issuing warp slows the arithmetic warps of its SM
+// sub-partition by 19 %, a single issuing lane by 2 %.
+#ifndef K4_LANE0_ISSUE
+#define K4_LANE0_ISSUE 1
+#endif
+
+template <uint32_t A_OFF, uint32_t B_OFF>
+__device__ __forceinline__ void k4_mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  if constexpr (K4_LANE0_ISSUE) mma_ss_off<A_OFF, B_OFF>(d, a, b, idesc, acc);
+  else mma_ss_e<A_OFF, B_OFF>(d, a, b, idesc, acc);
+}
+template <uint32_t A_COL, uint32_t B_OFF>
+__device__ __forceinline__ void k4_mma_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  if constexpr (K4_LANE0_ISSUE) mma_ts_off<A_COL, B_OFF>(d, a, b, idesc, acc);
+  else mma_ts_e<A_COL, B_OFF>(d, a, b, idesc, acc);
+}
+__device__ __forceinline__ void k4_commit(uint64_t* bar) {
+  if constexpr (K4_LANE0_ISSUE) mma_commit(bar);
+  else mma_commit_e(bar);
+}
 template <int D, int BN>
 struct Attn1Cfg {
   static constexpr int BM = 128;
@@ -543,10 +565,10 @@ __global__ void __launch_bounds__(Attn1Cfg<D, BN>::THREADS, 1)
     // K-major SW128: 32 bytes per K step inside a 128B atom, atoms one box apart (offsets in 16 B)
     static_for<D / 16>([&](auto kc) {
       constexpr int kk = decltype(kc)::value;
-      mma_ss_e<((kk / 4) * C::Q_BOX + (kk % 4) * 32) / 16, ((kk / 4) * C::KV_BOX + (kk % 4) * 32) / 16>(
+      k4_mma_ss<((kk / 4) * C::Q_BOX + (kk % 4) * 32) / 16, ((kk / 4) * C::KV_BOX + (kk % 4) * 32) / 16>(
           tmem + b * BN, a_base, b_base, C::IDESC_S, kk > 0 ? 1u : 0u);
     });
-    mma_commit_e(&s_full[b]);          // also releases K slot b to the producer
+    k4_commit(&s_full[b]);          // also releases K slot b to the producer
   };
   // PV_j: O += P_j V_j with P_j from TMEM (TS form)
   auto issue_pv = [&](int j, auto bc, auto vc) {
@@ -562,9 +584,9 @@ __global__ void __launch_bounds__(Attn1Cfg<D, BN>::THREADS, 1)
     const uint32_t acc0 = j > 0 ? 1u : 0u;
     static_for<BN / 16>([&](auto kc) {
       constexpr int kk = decltype(kc)::value;
-      mma_ts_e<kk * 8, kk * 2048 / 16>(tmem + C::TMEM_O, tmem + b * BN, v_base, C::IDESC_O, kk > 0 ? 1u : acc0);
+      k4_mma_ts<kk * 8, kk * 2048 / 16>(tmem + C::TMEM_O, tmem + b * BN, v_base, C::IDESC_O, kk > 0 ? 1u : acc0);
     });
-    mma_commit_e(&o_done[b]);          // also releases V slot vs to the producer
+    k4_commit(&o_done[b]);          // also releases V slot vs to the producer
     K4T(0, 3, j);
   };
   constexpr int UPV = (NS % 2) ? 2 * NS : NS;   // PV loops unrolled over lcm(NS, 2): literal slots
@@ -592,7 +614,7 @@ __global__ void __launch_bounds__(Attn1Cfg<D, BN>::THREADS, 1)
     }
   } else if (warp == 1 || warp == C::S_WARP) {
     // ------------------------------------------------------------ MMA issuers
-    if (L > 0) {
+    if (L > 0 && (!K4_LANE0_ISSUE || lane == 0)) {
       K4_WAIT(q_full, 0);
       tc_fence_after();
       if (warp == 1) {
@@ -862,10 +884,10 @@ __global__ void __launch_bounds__(WideCfg<D, BN>::THREADS, 1)
     const uint64_t b_base = smem_desc_sw128(smem_u32(smem + C::OFF_K + b * C::KV_BYTES), 16, 1024);
     static_for<D / 16>([&](auto kc) {
       constexpr int kk = decltype(kc)::value;
-      mma_ss_e<((kk / 4) * C::Q_BOX + (kk % 4) * 32) / 16, ((kk / 4) * C::KV_BOX + (kk % 4) * 32) / 16>(
+      k4_mma_ss<((kk / 4) * C::Q_BOX + (kk % 4) * 32) / 16, ((kk / 4) * C::KV_BOX + (kk % 4) * 32) / 16>(
           tmem + b * BN, a_base, b_base, C::IDESC_S, kk > 0 ? 1u : 0u);
     });
-    mma_commit_e(&s_full[b]);
+    k4_commit(&s_full[b]);
   };
   // PV^c_j: O_c += P_j[:, keys of half c] V_j[keys of half c, :]; P^c packed in that half's first KH/2 columns
   auto issue_pv = [&](int j, auto bc, auto vc) {
@@ -881,11 +903,11 @@ __global__ void __launch_bounds__(WideCfg<D, BN>::THREADS, 1)
       tc_fence_after();
       static_for<C::KH / 16>([&](auto kc) {
         constexpr int kk = decltype(kc)::value;
-        mma_ts_e<c * C::KH + kk * 8, (c * C::KH / 16 + kk) * 2048 / 16>(tmem + C::TMEM_O + c * D, tmem + b * BN,
+        k4_mma_ts<c * C::KH + kk * 8, (c * C::KH / 16 + kk) * 2048 / 16>(tmem + C::TMEM_O + c * D, tmem + b * BN,
                                                                         v_base, C::IDESC_O, kk > 0 ? 1u : acc0);
       });
     });
-    mma_commit_e(&o_done[b]);
+    k4_commit(&o_done[b]);
     K4T(0, 2, j);
     K4T(0, 3, j);
   };
@@ -911,7 +933,7 @@ __global__ void __launch_bounds__(WideCfg<D, BN>::THREADS, 1)
       }
     }
   } else if (warp == 1 || warp == C::S_WARP) {
-    if (L > 0) {
+    if (L > 0 && (!K4_LANE0_ISSUE || lane == 0)) {
       K4_WAIT(q_full, 0);
       tc_fence_after();
       if (warp == 1) {
