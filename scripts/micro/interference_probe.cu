@@ -9,6 +9,8 @@
 //   mode 3  try_wait polling on a barrier that never completes (a waiting issuer)
 //   mode 4  try_wait with a suspend-time hint on a barrier that never completes
 //   mode 5  one MMA group every ~2000 cycles (light issue)
+//   mode 6  one lane streaming bulk copies global -> shared (4 x 16 KB per round, waiting on each round)
+//   mode 7  the same from a converged warp (elect one lane per copy)
 #include <cstdio>
 #include <cstdint>
 #include "../../paper_2601_11641_b200/csrc/sm100.cuh"
@@ -19,11 +21,11 @@ constexpr uint32_t IDESC_O = idesc_bf16_f32(128, 128, false, true);
 constexpr int TILE = 32768;
 
 template <int MODE>
-__global__ void __launch_bounds__(320, 1) probe(float* out, int iters) {
+__global__ void __launch_bounds__(320, 1) probe(float* out, int iters, const unsigned char* __restrict__ gsrc) {
   extern __shared__ __align__(1024) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 3 * TILE);
-  uint32_t* slot = reinterpret_cast<uint32_t*>(bars + 4);
-  volatile int* stop = reinterpret_cast<volatile int*>(bars + 5);
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bars + 5);
+  volatile int* stop = reinterpret_cast<volatile int*>(bars + 6);
   __shared__ long long cyc[8];
   __shared__ int ndone;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -33,6 +35,7 @@ __global__ void __launch_bounds__(320, 1) probe(float* out, int iters) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
     mbar_init(&bars[2], 1);   // never completes
+    mbar_init(&bars[3], 1);   // bulk-copy rounds (modes 6, 7)
     *stop = 0;
     ndone = 0;
     fence_mbar_init();
@@ -121,6 +124,23 @@ __global__ void __launch_bounds__(320, 1) probe(float* out, int iters) {
         mma_commit_e(&bars[j & 1]);
         __syncwarp();
       }
+    } else if (MODE == 6 || MODE == 7) {
+      uint32_t ph = 0;
+      for (int it = 0; !*stop; ++it) {
+        if (MODE == 6 && lane != 0) break;
+        const unsigned char* src = gsrc + (size_t)((blockIdx.x * 7 + it) % 64) * 4 * 16384;
+        if (lane == 0) mbar_arrive_expect_tx(&bars[3], 4 * 16384);
+        if (MODE == 7) __syncwarp();
+        for (int c = 0; c < 4; ++c) {
+          const bool me = MODE == 6 ? true : elect_one();
+          if (me)
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         ::"r"(smem_u32(smem + 16384 * c)), "l"(src + 16384 * c), "r"(16384), "r"(smem_u32(&bars[3]))
+                         : "memory");
+        }
+        mbar_wait_sleep(&bars[3], ph);
+        ph ^= 1;
+      }
     } else if (MODE == 3 || MODE == 4) {
       if (lane == 0) {
         while (!*stop) {
@@ -149,14 +169,19 @@ __global__ void __launch_bounds__(320, 1) probe(float* out, int iters) {
 
 template <int MODE>
 void run(const char* name, int sms) {
+  static unsigned char* g = nullptr;
+  if (!g) {
+    cudaMalloc(&g, 64ull * 4 * 16384);
+    cudaMemset(g, 0, 64ull * 4 * 16384);
+  }
   float* d;
   cudaMalloc(&d, 5 * sizeof(float));
   cudaMemset(d, 0, 5 * sizeof(float));
-  const int smem = 3 * TILE + 64;
+  const int smem = 3 * TILE + 128;
   cudaFuncSetAttribute(probe<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  probe<MODE><<<sms, 320, smem>>>(d, 200);   // warm-up
+  probe<MODE><<<sms, 320, smem>>>(d, 200, g);   // warm-up
   cudaMemset(d, 0, 5 * sizeof(float));
-  probe<MODE><<<sms, 320, smem>>>(d, 2000);
+  probe<MODE><<<sms, 320, smem>>>(d, 2000, g);
   cudaError_t e = cudaDeviceSynchronize();
   float h[5];
   cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
@@ -174,6 +199,8 @@ int main() {
   run<3>("try_wait polling", sms);
   run<4>("try_wait with suspend hint", sms);
   run<5>("light MMA issue (1 group / 2000 cycles)", sms);
+  run<6>("one lane streaming bulk copies", sms);
+  run<7>("converged warp streaming bulk copies", sms);
   run<0>("issuer idle (again)", sms);
   return 0;
 }
