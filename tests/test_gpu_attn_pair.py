@@ -31,7 +31,7 @@ def M():
     return m
 
 
-KERNELS = ["default", "splitkv", "pair", "wide"]
+KERNELS = ["default", "splitkv", "pair", "wide", "persist"]
 
 
 @pytest.fixture(params=KERNELS)
@@ -153,7 +153,7 @@ def test_variant_deterministic(M, kern):
     assert torch.equal(o1, o2) and torch.equal(l1, l2)
 
 
-@pytest.mark.parametrize("kern", ["default", "splitkv"])
+@pytest.mark.parametrize("kern", ["default", "splitkv", "persist"])
 @pytest.mark.parametrize("w", [syn.TINY, syn.Workload("b64-d128", 1, 2, 128, 0, 2, 10, 13, 64)], ids=lambda w: w.name)
 def test_block64(M, kern, w):
     """64-token blocks (the tiny config, D = 64; and D = 128): more S buffers, half-width softmax rows."""
@@ -186,6 +186,28 @@ def test_row_maximum_jumps(M, kern):
     rng = np.random.default_rng(13)
     masks = rng.random((1, w.heads, L.n, L.n)) < 0.7
     masks[0, 0, 0] = True
+    rp, ci = masks_to_csr(masks)
+    o, lse = P.block_sparse_attn_fwd(q, k, v, rp, ci)
+    torch.cuda.synchronize()
+    _check(o, lse, masks, q, k, v, L)
+
+
+@pytest.mark.parametrize("kern", KERNELS)
+@pytest.mark.parametrize("stride", [3, 13])
+def test_runs_of_empty_rows(M, kern, stride):
+    """Only every stride-th query block has a list (long runs of empty rows: the persistent schedule's
+    item ring then runs more than its depth ahead of the softmax and must keep issuing the V loads it
+    owes); the listed rows are long and the empty ones must still come out as O = 0, lse = -inf (Z15)."""
+    w = COG_SMALL
+    L = olayout(w)
+    P = M.Plan(w, attn_kernel=kern)
+    q, k, v = syn.family_r(w, seed=715, device="cuda")
+    rng = np.random.default_rng(stride)
+    masks = np.zeros((1, w.heads, L.n, L.n), dtype=bool)
+    for h in range(w.heads):
+        for i in range(h, L.n, stride):
+            masks[0, h, i] = rng.random(L.n) < 0.5
+            masks[0, h, i, i] = True
     rp, ci = masks_to_csr(masks)
     o, lse = P.block_sparse_attn_fwd(q, k, v, rp, ci)
     torch.cuda.synchronize()
