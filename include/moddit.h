@@ -78,10 +78,7 @@ typedef enum {
                                blocks: the WIDE schedule (measured faster there) */
   MOD_ATTN_SPLITKV = 1,     /* two 4-warp softmax groups splitting the index list (round-1 kernel) */
   MOD_ATTN_PAIR = 2,        /* two query blocks per CTA walking their merged index list (f4) */
-  MOD_ATTN_WIDE = 3,        /* 16 softmax warps, split-KV over the two key halves of each block (128-token blocks) */
-  MOD_ATTN_PERSIST = 4      /* the DEFAULT roles and softmax in one persistent CTA per SM over query-block items
-                               fetched from an atomic counter (item fill / drain overlap the neighbours' steady
-                               state; uses 16 bytes of ws, zeroed on the stream before each launch) */
+  MOD_ATTN_WIDE = 3         /* 16 softmax warps, split-KV over the two key halves of each block (128-token blocks) */
 } mod_attn_kernel;
 
 typedef struct {

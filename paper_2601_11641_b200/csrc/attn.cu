@@ -776,423 +776,6 @@ __global__ void __launch_bounds__(Attn1Cfg<D, BN>::THREADS, 1)
 }
 
 // ================================================================================================
-// Persistent K4 schedule (MOD_ATTN_PERSIST): the default schedule's roles and softmax, run by ONE CTA
-// per SM over a stream of query-block items fetched from an atomic counter, so that an item's pipeline
-// fill (Q load, first K/V loads, first S) and drain (last PV, O readout and store) overlap its
-// neighbours' steady state instead of costing every (b, h, query block) a CTA launch, barrier / TMEM set-up
-// and an empty tensor pipe (≈ 4.7 µs per CTA measured in the one-CTA-per-item schedule: 21 % of K4 on the
-// ≈ 17-block lists of CogVideoX-5B).
-//   warp 0      item fetcher + Q / K producer: fetches item t+1 (atomicAdd) while item t's loads go out,
-//               posts each item {id, list begin, L} into a shared ring read by every other role; Q into
-//               slot tq % 2 (tq = index among non-empty items), K of the global block stream g into
-//               slot g % NS.
-//   warp 11     V producer: V of global block g into slot g % 2.
-//   warp 10     S issuer: S_g = Q_tq K_g^T into TMEM buffer g % NS once PV_{g-NS} has completed; after an
-//               item's last S it commits q_empty[tq % 2].
-//   warp 1      TMEM allocator + PV issuer: O[tq % OB] (+)= P_g V_g; before an item's first PV it waits
-//               o_free (the epilogue of item tq - OB has read that accumulator); after its last PV it
-//               commits o_full[tq % OB].
-//   warps 2..9  softmax exactly as attn_fwd_kernel (16 rows per warp, lazy reference max); per item the
-//               epilogue reads O[tq % OB] into registers, releases it (o_free), then normalises and stores.
-// Every barrier phase follows from the global block counter g or the non-empty item counter tq, which
-// all roles advance identically, and every wait is on a phase whose successor needs the waiter's own
-// later work (the same argument as attn_fwd_kernel, across item boundaries).
-// TMEM: S[b] at b BN (b < NS), O[ob] after them; OB = 2 accumulators where they fit (D = 64: the next
-// item's first PV does not wait for the previous epilogue), else 1.
-// K4_PERSIST_VWARP = 1: V loads in a warp of their own (12 warps); 0: the Q / K producer thread also issues
-// the V loads, NS blocks behind its K loads (the one-CTA-per-item schedule's demand order; 11 warps)
-#ifndef K4_PERSIST_VWARP
-#define K4_PERSIST_VWARP 0
-#endif
-template <int D, int BN>
-struct PersistCfg {
-  static constexpr int BM = 128;
-  static constexpr int OB = (3 * BN + 2 * D) <= 512 ? 2 : 1;
-  static constexpr int NS = (512 - OB * D) / BN > 7 ? 7 : (512 - OB * D) / BN;
-  static constexpr int IR = 8;                        // item ring depth
-  static constexpr int COLS = BN / 2, OCOLS = D / 2;
-  static constexpr int Q_BOX = BM * 128, KV_BOX = BN * 128, NATOM = D / 64;
-  static constexpr int Q_BYTES = Q_BOX * NATOM, KV_BYTES = KV_BOX * NATOM;
-  static constexpr int OFF_Q = 0;                     // 2 Q slots
-  static constexpr int OFF_K = OFF_Q + 2 * Q_BYTES;
-  static constexpr int OFF_V = OFF_K + NS * KV_BYTES;
-  static constexpr int OFF_BAR = OFF_V + 2 * KV_BYTES;
-  // q_full[2] q_empty[2] k_full[NS] v_full[2] s_full[NS] p_full[NS] o_done[NS] o_full[OB] o_free[OB]
-  // item_full[IR] item_empty[IR]
-  static constexpr int NUM_BARS = 2 + 2 + NS + 2 + NS + NS + NS + OB + OB + IR + IR;
-  static constexpr int OFF_RING = (OFF_BAR + NUM_BARS * 8 + 16 + 15) / 16 * 16;
-  static constexpr int SMEM = OFF_RING + IR * 16 + 8 * 8;
-  static constexpr int TMEM_O = NS * BN;
-  static constexpr uint32_t TMEM_COLS = (NS * BN + OB * D) <= 256 ? 256 : 512;
-  static constexpr int SOFTMAX_WARPS = 8;
-  static constexpr int S_WARP = 2 + SOFTMAX_WARPS, V_WARP = K4_PERSIST_VWARP ? S_WARP + 1 : -1;
-  static constexpr int THREADS = 32 * (S_WARP + 1 + (K4_PERSIST_VWARP ? 1 : 0));
-  // ring readers: S, PV, softmax warps (+ the V producer warp)
-  static constexpr int CONSUMERS = 2 + SOFTMAX_WARPS + (K4_PERSIST_VWARP ? 1 : 0);
-  static constexpr int OFF_VQ = OFF_RING + IR * 16;   // producer's (bh, row) of loaded K blocks awaiting V [8]
-  static constexpr uint32_t IDESC_S = idesc_bf16_f32(BM, BN, false, false);
-  static constexpr uint32_t IDESC_O = idesc_bf16_f32(BM, D, false, true);
-  static constexpr int EMU = Attn1Cfg<D, BN>::EMU;
-  static constexpr float OVF = 1048576.0f;
-  static_assert(SMEM <= 232448, "PersistCfg: shared memory");
-};
-
-template <int D, int BN>
-__global__ void __launch_bounds__(PersistCfg<D, BN>::THREADS, 1)
-    attn_persist_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                        const __grid_constant__ CUtensorMap tm_v, const int* __restrict__ row_ptr,
-                        const int* __restrict__ col_idx, __nv_bfloat16* __restrict__ out, float* __restrict__ lse,
-                        int N, int n, int block, float scale_log2, int* __restrict__ sched, int total) {
-  using C = PersistCfg<D, BN>;
-  constexpr int NS = C::NS, OB = C::OB, IR = C::IR;
-  extern __shared__ __align__(1024) unsigned char smem[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
-  uint64_t* q_full = bars;
-  uint64_t* q_empty = q_full + 2;
-  uint64_t* k_full = q_empty + 2;
-  uint64_t* v_full = k_full + NS;
-  uint64_t* s_full = v_full + 2;
-  uint64_t* p_full = s_full + NS;
-  uint64_t* o_done = p_full + NS;
-  uint64_t* o_full = o_done + NS;
-  uint64_t* o_free = o_full + OB;
-  uint64_t* item_full = o_free + OB;
-  uint64_t* item_empty = item_full + IR;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(item_empty + IR);
-  int4* ring = reinterpret_cast<int4*>(smem + C::OFF_RING);
-
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  if (threadIdx.x == 0 && (smem_u32(smem) & 1023u) != 0) __trap();   // SWIZZLE_128B needs 1024B alignment
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&q_full[s], 1);
-      mbar_init(&q_empty[s], 1);
-      mbar_init(&v_full[s], 1);
-    }
-    for (int s = 0; s < NS; ++s) {
-      mbar_init(&k_full[s], 1);
-      mbar_init(&s_full[s], 1);
-      mbar_init(&p_full[s], C::SOFTMAX_WARPS);
-      mbar_init(&o_done[s], 1);
-    }
-    for (int s = 0; s < OB; ++s) {
-      mbar_init(&o_full[s], 1);
-      mbar_init(&o_free[s], C::SOFTMAX_WARPS);
-    }
-    for (int r = 0; r < IR; ++r) {
-      mbar_init(&item_full[r], 1);
-      mbar_init(&item_empty[r], C::CONSUMERS);
-    }
-    fence_mbar_init();
-  }
-  if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const size_t nn = (size_t)n * n;
-
-  // next item record of the ring (every reader, in order); one arrival per reading warp
-  auto read_item = [&](int t, bool arrive) -> int4 {
-    const int r = t % IR;
-    mbar_wait(&item_full[r], (uint32_t)(t / IR) & 1u);
-    const int4 rec = ring[r];
-    if (arrive) mbar_arrive(&item_empty[r]);
-    return rec;
-  };
-  const uint64_t pol_kv = policy_evict_last();
-
-  if (warp == 0) {
-    // ------------------------------------------------------------ item fetcher + Q / K (/ V) producer
-    if (lane == 0) {
-      tma_prefetch_desc(&tm_q);
-      tma_prefetch_desc(&tm_k);
-      tma_prefetch_desc(&tm_v);
-      const uint64_t pol_q = policy_evict_first();
-      int2* vq = reinterpret_cast<int2*>(smem + C::OFF_VQ);   // (bh, first key row) of K blocks awaiting V
-      int nxt = atomicAdd(sched, 1);
-      int t = 0, tq = 0, gk = 0, gv = 0, Lk = 0, jk = 0, bhk = 0;
-      const int* colsk = col_idx;
-      bool done = false;
-      auto load_v = [&]() {   // V of global block gv into slot gv % 2
-        const int vs = gv & 1;
-        if (gv >= 2) K4_WAIT(&o_done[(gv - 2) % NS], (uint32_t)((gv - 2) / NS) & 1u);   // PV_{g-2} read slot vs
-        const int2 e = vq[gv & 7];
-        unsigned char* dst = smem + C::OFF_V + vs * C::KV_BYTES;
-        mbar_arrive_expect_tx(&v_full[vs], C::KV_BYTES);
-#pragma unroll
-        for (int a = 0; a < C::NATOM; ++a) tma_load_3d(dst + a * C::KV_BOX, &tm_v, &v_full[vs], a * 64, e.y, e.x, pol_kv);
-        ++gv;
-      };
-      // K of the next block of the item stream (posting items and loading Q as the cursor enters them);
-      // false once the stream is exhausted
-      auto advance_k = [&]() -> bool {
-        while (jk >= Lk) {
-          if (done) return false;
-          const int r = t % IR;
-          if (t >= IR) {
-            const uint32_t ph = (uint32_t)(t / IR - 1) & 1u;
-            // readers still on item t-IR (possible only behind a run of empty items): their progress may
-            // need V loads this thread still owes, so issue those while waiting
-            while (!mbar_test(&item_empty[r], ph)) {
-              if (!K4_PERSIST_VWARP && gv < gk) load_v();
-              else { K4_WAIT(&item_empty[r], ph); break; }
-            }
-          }
-          const int it = nxt;
-          int4 rec = make_int4(-1, 0, 0, 0);
-          if (it < total) {
-            const int bh = it / n, qi = it % n;
-            const int beg = row_ptr[(size_t)bh * (n + 1) + qi];
-            rec = make_int4(it, beg, row_ptr[(size_t)bh * (n + 1) + qi + 1] - beg, 0);
-            nxt = atomicAdd(sched, 1);   // the following item, fetched while this one's loads go out
-          }
-          ring[r] = rec;
-          mbar_arrive(&item_full[r]);    // release: the record is visible to the waiting readers
-          ++t;
-          if (it >= total) { done = true; return false; }
-          if (rec.z == 0) continue;
-          const int bh = it / n, qi = it % n;
-          const int qs = tq & 1;
-          if (tq >= 2) K4_WAIT(&q_empty[qs], (uint32_t)((tq - 2) >> 1) & 1u);   // S of item tq-2 done with slot qs
-          mbar_arrive_expect_tx(&q_full[qs], C::Q_BYTES);
-#pragma unroll
-          for (int a = 0; a < C::NATOM; ++a)
-            tma_load_3d(smem + C::OFF_Q + qs * C::Q_BYTES + a * C::Q_BOX, &tm_q, &q_full[qs], a * 64, qi * block, bh, pol_q);
-          Lk = rec.z;
-          jk = 0;
-          bhk = bh;
-          colsk = col_idx + (size_t)bh * nn + rec.y;
-          ++tq;
-        }
-        const int b = gk % NS;
-        if (gk >= NS) K4_WAIT(&s_full[b], (uint32_t)(gk / NS - 1) & 1u);   // S_{g-NS} consumed K slot b
-        const int row = colsk[jk] * block;
-        vq[gk & 7] = make_int2(bhk, row);
-        unsigned char* dst = smem + C::OFF_K + b * C::KV_BYTES;
-        mbar_arrive_expect_tx(&k_full[b], C::KV_BYTES);
-#pragma unroll
-        for (int a = 0; a < C::NATOM; ++a) tma_load_3d(dst + a * C::KV_BOX, &tm_k, &k_full[b], a * 64, row, bhk, pol_kv);
-        ++gk;
-        ++jk;
-        return true;
-      };
-      if constexpr (K4_PERSIST_VWARP) {
-        while (advance_k()) {
-        }
-      } else {
-        // demand order of the MMA warps: K_0 .. K_{NS-1}, then V_g, K_{g+NS} for g = 0, 1, ...
-        for (int i = 0; i < NS; ++i)
-          if (!advance_k()) break;
-        while (gv < gk) {
-          load_v();
-          advance_k();
-        }
-      }
-    }
-  } else if (K4_PERSIST_VWARP && warp == C::V_WARP) {
-    // ------------------------------------------------------------ V producer
-    if (lane == 0) {
-      int gv = 0;
-      for (int t = 0;; ++t) {
-        const int4 rec = read_item(t, true);
-        if (rec.x < 0) break;
-        const int L = rec.z;
-        const int bh = rec.x / n;
-        const int* cols = col_idx + (size_t)bh * nn + rec.y;
-        for (int j = 0; j < L; ++j, ++gv) {
-          const int vs = gv & 1;
-          if (gv >= 2) K4_WAIT(&o_done[(gv - 2) % NS], (uint32_t)((gv - 2) / NS) & 1u);   // PV_{g-2} read slot vs
-          unsigned char* dst = smem + C::OFF_V + vs * C::KV_BYTES;
-          mbar_arrive_expect_tx(&v_full[vs], C::KV_BYTES);
-          const int row = cols[j] * block;
-#pragma unroll
-          for (int a = 0; a < C::NATOM; ++a) tma_load_3d(dst + a * C::KV_BOX, &tm_v, &v_full[vs], a * 64, row, bh, pol_kv);
-        }
-      }
-    }
-  } else if (warp == C::S_WARP) {
-    // ------------------------------------------------------------ S issuer
-    if (lane == 0) {
-      int g = 0, tq = 0;
-      for (int t = 0;; ++t) {
-        const int4 rec = read_item(t, true);
-        if (rec.x < 0) break;
-        const int L = rec.z;
-        if (L == 0) continue;
-        const int qs = tq & 1;
-        K4_WAIT(&q_full[qs], (uint32_t)(tq >> 1) & 1u);
-        const uint64_t a_base = smem_desc_sw128(smem_u32(smem + C::OFF_Q + qs * C::Q_BYTES), 16, 1024);
-        for (int j = 0; j < L; ++j, ++g) {
-          const int b = g % NS;
-          if (g >= NS) K4_WAIT(&o_done[b], (uint32_t)(g / NS - 1) & 1u);   // PV_{g-NS} has read P from S[b]
-          K4_WAIT(&k_full[b], (uint32_t)(g / NS) & 1u);
-          tc_fence_after();
-          const uint64_t b_base = smem_desc_sw128(smem_u32(smem + C::OFF_K + b * C::KV_BYTES), 16, 1024);
-          static_for<D / 16>([&](auto kc) {
-            constexpr int kk = decltype(kc)::value;
-            k4_mma_ss<((kk / 4) * C::Q_BOX + (kk % 4) * 32) / 16, ((kk / 4) * C::KV_BOX + (kk % 4) * 32) / 16>(
-                tmem + b * BN, a_base, b_base, C::IDESC_S, kk > 0 ? 1u : 0u);
-          });
-          k4_commit(&s_full[b]);   // also releases K slot b to the producer
-        }
-        k4_commit(&q_empty[qs]);   // the item's S MMAs have read Q slot qs once they complete
-        ++tq;
-      }
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ PV issuer
-    if (lane == 0) {
-      int g = 0, tq = 0;
-      for (int t = 0;; ++t) {
-        const int4 rec = read_item(t, true);
-        if (rec.x < 0) break;
-        const int L = rec.z;
-        if (L == 0) continue;
-        const int ob = tq % OB;
-        const uint32_t d_o = tmem + C::TMEM_O + ob * D;
-        for (int j = 0; j < L; ++j, ++g) {
-          const int b = g % NS, vs = g & 1;
-          K4_WAIT(&v_full[vs], (uint32_t)(g >> 1) & 1u);
-          K4_WAIT(&p_full[b], (uint32_t)(g / NS) & 1u);
-          if (j == 0 && tq >= OB) K4_WAIT(&o_free[ob], (uint32_t)(tq / OB - 1) & 1u);   // epilogue of item tq-OB
-          tc_fence_after();
-          const uint64_t v_base = smem_desc_sw128(smem_u32(smem + C::OFF_V + vs * C::KV_BYTES), C::KV_BOX, 1024);
-          const uint32_t acc0 = j > 0 ? 1u : 0u;
-          static_for<BN / 16>([&](auto kc) {
-            constexpr int kk = decltype(kc)::value;
-            k4_mma_ts<kk * 8, kk * 2048 / 16>(d_o, tmem + b * BN, v_base, C::IDESC_O, kk > 0 ? 1u : acc0);
-          });
-          k4_commit(&o_done[b]);   // also releases V slot vs to the V producer
-        }
-        k4_commit(&o_full[ob]);
-        ++tq;
-      }
-    }
-  } else {
-    // ------------------------------------------------------------ softmax / epilogue (8 independent warps)
-    constexpr int COLS = C::COLS, OCOLS = C::OCOLS;
-    constexpr unsigned FULL = 0xffffffffu;
-    const int quarter = warp & 3;
-    const int h = (warp - 2) >> 2;
-    const int half = lane >> 4;
-    const int rloc = quarter * 32 + h * 16 + (lane & 15);   // query row within the tile
-    const uint32_t lane_off = (uint32_t)(quarter * 32 + h * 16) << 16;
-    int g = 0, tq = 0;
-#pragma unroll 1
-    for (int t = 0;; ++t) {
-      const int4 rec = read_item(t, false);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&item_empty[t % IR]);
-      if (rec.x < 0) break;
-      const int it = rec.x, L = rec.z;
-      const int bh = it / n, qi = it % n;
-      const int q_row0 = qi * block;
-      const bool valid = rloc < min(block, N - q_row0);
-      const size_t grow = (size_t)bh * N + q_row0 + rloc;
-      if (L == 0) {
-        if (valid) {
-          int4* dst = reinterpret_cast<int4*>(out + grow * D + half * OCOLS);
-#pragma unroll
-          for (int e = 0; e < OCOLS / 8; ++e) dst[e] = make_int4(0, 0, 0, 0);
-          if (lse && half == 0) lse[grow] = -INFINITY;
-        }
-        continue;
-      }
-      const int* cols = col_idx + (size_t)bh * nn + rec.y;
-      const int ob = tq % OB;
-      const uint32_t t_o = tmem + lane_off + C::TMEM_O + ob * D;
-      float m_run = -INFINITY, l_run = 0.f;
-      int col_next = cols[0];
-#pragma unroll 1
-      for (int j = 0; j < L; ++j, ++g) {
-        const int b = g % NS;
-        const int col = col_next;
-        if (j + 1 < L) col_next = cols[j + 1];
-        K4_SWAIT(&s_full[b], (uint32_t)(g / NS) & 1u);
-        tc_fence_after();
-        uint32_t sr[COLS];
-        tmem_ld_rows<COLS, BN / 2>(tmem + lane_off + b * BN, sr);
-        tmem_ld_wait();
-        float* s = reinterpret_cast<float*>(sr);
-        const int kv_valid = N - col * block - half * COLS;
-        if (kv_valid < COLS) {
-#pragma unroll
-          for (int c = 0; c < COLS; ++c)
-            if (c >= kv_valid) s[c] = -INFINITY;
-        }
-        if (j == 0) {
-          const float mx = row_max<COLS>(s) * scale_log2;
-          m_run = fmaxf(mx, __shfl_xor_sync(FULL, mx, 16));
-        }
-        uint32_t pk[COLS / 2];
-        float sum = exp_pack<C::EMU, COLS>(s, scale_log2, m_run, pk);
-        const bool need = !(sum <= C::OVF);
-        if (__any_sync(FULL, need)) {
-          const int need_peer = __shfl_xor_sync(FULL, (int)need, 16);
-          const bool need_row = need || need_peer != 0;
-          float rmax = row_max<COLS>(s) * scale_log2;
-          rmax = fmaxf(rmax, __shfl_xor_sync(FULL, rmax, 16));
-          const float m_new = need_row ? fmaxf(m_run, rmax) : m_run;
-          const float alpha = ex2(m_run - m_new);
-          if (need_row) sum = exp_pack<0, COLS>(s, scale_log2, m_new, pk);
-          l_run *= alpha;
-          m_run = m_new;
-          if (j > 0 && __any_sync(FULL, alpha < 1.f)) {
-            mbar_wait(&o_done[(g - 1) % NS], (uint32_t)((g - 1) / NS) & 1u);   // PV_{g-1} has written O[ob]
-            tc_fence_after();
-            constexpr int OCH = OCOLS < 32 ? OCOLS : 32;
-#pragma unroll
-            for (int c = 0; c < OCOLS / OCH; ++c) {
-              uint32_t o[OCH];
-              tmem_ld_rows<OCH, D / 2>(t_o + c * OCH, o);
-              tmem_ld_wait();
-#pragma unroll
-              for (int e = 0; e < OCH; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-              tmem_st_rows<OCH, D / 2>(t_o + c * OCH, o);
-            }
-          }
-        }
-        l_run += sum;
-        tmem_st_rows<COLS / 2, BN / 4>(tmem + lane_off + b * BN, pk);
-        tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[b]);
-      }
-      // epilogue: read O[ob] out, release it to the next item's PV, then O / l -> bf16 and lse
-      const float l = l_run + __shfl_xor_sync(FULL, l_run, 16);
-      mbar_wait(&o_full[ob], (uint32_t)(tq / OB) & 1u);
-      tc_fence_after();
-      uint32_t o[OCOLS];
-      tmem_ld_rows<OCOLS, D / 2>(t_o, o);
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&o_free[ob]);
-      const float inv = 1.0f / l;
-      if (valid) {
-        int4* dst = reinterpret_cast<int4*>(out + grow * D + half * OCOLS);
-#pragma unroll
-        for (int e = 0; e < OCOLS / 8; ++e)
-          dst[e] = make_int4(pack_bf16(__uint_as_float(o[8 * e]) * inv, __uint_as_float(o[8 * e + 1]) * inv),
-                             pack_bf16(__uint_as_float(o[8 * e + 2]) * inv, __uint_as_float(o[8 * e + 3]) * inv),
-                             pack_bf16(__uint_as_float(o[8 * e + 4]) * inv, __uint_as_float(o[8 * e + 5]) * inv),
-                             pack_bf16(__uint_as_float(o[8 * e + 6]) * inv, __uint_as_float(o[8 * e + 7]) * inv));
-        if (lse && half == 0) lse[grow] = (m_run + __log2f(l)) * 0.69314718055994531f;
-      }
-      ++tq;
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc<C::TMEM_COLS>(tmem);
-  }
-}
-
-// ================================================================================================
 // Wide K4 schedule (MOD_ATTN_WIDE, 128-token blocks): FOUR softmax warps per SM sub-partition.
 // ncu of the default schedule shows ~0.7 eligible warps per scheduler and 50 % issue utilisation: the
 // softmax is latency-bound with two warps per sub-partition.  Here warp (quarter q, half h, key half c)
@@ -1884,31 +1467,6 @@ mod_status launch_split(mod_plan P, const void* q, const void* k, const void* v,
   return launch_rows<SplitCfg<D, BN>>(P, attn_split_kernel<D, BN>, D, BN, q, k, v, row_ptr, col_idx, o, lse, s);
 }
 
-// Persistent schedule: one CTA per SM (fewer for tiny problems), the item counter in ws zeroed on the stream
-template <int D, int BN>
-mod_status launch_persist(mod_plan P, const void* q, const void* k, const void* v, const int* row_ptr,
-                          const int* col_idx, void* o, float* lse, void* ws, cudaStream_t s) {
-  using Cfg = PersistCfg<D, BN>;
-  MOD_REQUIRE(ws, MOD_ERR_USAGE, "mod_block_sparse_attn_fwd: the persistent schedule needs the plan workspace");
-  const int BH = P->L.batch * P->L.heads;
-  CUtensorMap tq, tk, tv;
-  mod_status st;
-  if ((st = make_map(&tq, q, BH, P->N, D, Cfg::BM)) != MOD_OK) return st;
-  if ((st = make_map(&tk, k, BH, P->N, D, BN)) != MOD_OK) return st;
-  if ((st = make_map(&tv, v, BH, P->N, D, BN)) != MOD_OK) return st;
-  auto kern = attn_persist_kernel<D, BN>;
-  MOD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-  int* sched = reinterpret_cast<int*>(static_cast<unsigned char*>(ws) + P->ws_sched);
-  MOD_CUDA(cudaMemsetAsync(sched, 0, sizeof(int), s));
-  const float scale_log2 = P->scale * 1.4426950408889634f;
-  const int total = BH * P->n;
-  const int grid = total < P->sm_count ? total : P->sm_count;
-  kern<<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(tq, tk, tv, row_ptr, col_idx, (__nv_bfloat16*)o, lse, P->N, P->n,
-                                            P->L.block, scale_log2, sched, total);
-  MOD_LAUNCH_CHECK();
-  return MOD_OK;
-}
-
 template <int D>
 mod_status launch_pair(mod_plan P, const void* q, const void* k, const void* v, const int* row_ptr, const int* col_idx,
                        void* o, float* lse, cudaStream_t s) {
@@ -1945,10 +1503,7 @@ int effective_kernel(mod_plan P) {
   // the kernel; the wide schedule's four softmax warps per sub-partition hide its latencies better there
   // (CogVideoX-5B: 598 vs 559 TFLOP/s), while at D = 128 the 8-warp schedule with three S buffers is faster
   // (1212 vs 1161 TFLOP/s at Hunyuan; profiles/r2/README.md)
-#ifndef K4_D64_WIDE
-#define K4_D64_WIDE 1
-#endif
-  if (K4_D64_WIDE && want == MOD_ATTN_DEFAULT && P->L.head_dim == 64 && P->L.block == 128) return MOD_ATTN_WIDE;
+  if (want == MOD_ATTN_DEFAULT && P->L.head_dim == 64 && P->L.block == 128) return MOD_ATTN_WIDE;
   return want;
 }
 }  // namespace
@@ -1972,9 +1527,6 @@ extern "C" const char* mod_attn_kernel_name(mod_plan P) {
                       : (BN == 128 ? "attn_split_kernel<64,128>" : "attn_split_kernel<64,64>");
     case MOD_ATTN_PAIR: return D == 128 ? "attn_pair_kernel<128,128>" : "attn_pair_kernel<64,128>";
     case MOD_ATTN_WIDE: return D == 128 ? "attn_wide_kernel<128,128>" : "attn_wide_kernel<64,128>";
-    case MOD_ATTN_PERSIST:
-      return D == 128 ? (BN == 128 ? "attn_persist_kernel<128,128>" : "attn_persist_kernel<128,64>")
-                      : (BN == 128 ? "attn_persist_kernel<64,128>" : "attn_persist_kernel<64,64>");
     default:
       return D == 128 ? (BN == 128 ? "attn_fwd_kernel<128,128>" : "attn_fwd_kernel<128,64>")
                       : (BN == 128 ? "attn_fwd_kernel<64,128>" : "attn_fwd_kernel<64,64>");
@@ -1985,6 +1537,7 @@ extern "C" mod_status mod_block_sparse_attn_fwd(mod_plan P, const void* q, const
                                                 const int32_t* row_ptr, const int32_t* col_idx, void* o, float* lse,
                                                 void* ws, void* stream) {
   MOD_NVTX("mod_block_sparse_attn_fwd");
+  (void)ws;
   mod_status st = mod_validate_plan(P);
   if (st != MOD_OK) return st;
   MOD_REQUIRE(q && k && v && row_ptr && col_idx && o, MOD_ERR_USAGE,
@@ -2000,12 +1553,6 @@ extern "C" mod_status mod_block_sparse_attn_fwd(mod_plan P, const void* q, const
     case MOD_ATTN_WIDE:
       st = D == 128 ? launch_wide<128, 128>(P, q, k, v, row_ptr, col_idx, o, lse, s)
                     : launch_wide<64, 128>(P, q, k, v, row_ptr, col_idx, o, lse, s);
-      break;
-    case MOD_ATTN_PERSIST:
-      if (D == 128 && BN == 128) st = launch_persist<128, 128>(P, q, k, v, row_ptr, col_idx, o, lse, ws, s);
-      else if (D == 64 && BN == 128) st = launch_persist<64, 128>(P, q, k, v, row_ptr, col_idx, o, lse, ws, s);
-      else if (D == 128 && BN == 64) st = launch_persist<128, 64>(P, q, k, v, row_ptr, col_idx, o, lse, ws, s);
-      else st = launch_persist<64, 64>(P, q, k, v, row_ptr, col_idx, o, lse, ws, s);
       break;
     case MOD_ATTN_SPLITKV:
       if (D == 128 && BN == 128) st = launch_split<128, 128>(P, q, k, v, row_ptr, col_idx, o, lse, s);

@@ -58,7 +58,7 @@ struct mod_plan_s {
   CUtensorMap tm_ginv;          // 2D TMA map over d_ginv: {ld, p} fp64, box {128 columns, 32 rows}
   size_t ws_bytes;
   // workspace carve (byte offsets)
-  size_t ws_qbar, ws_kbar, ws_qs, ws_ks, ws_part, ws_r, ws_x, ws_nae, ws_sel, ws_cnt, ws_solve, ws_sched;
+  size_t ws_qbar, ws_kbar, ws_qs, ws_ks, ws_part, ws_r, ws_x, ws_nae, ws_sel, ws_cnt, ws_solve;
   int proj_tiles, proj_rows;    // row tiles of the projection kernel / map rows per tile (<= 32, in smem)
   int solve_segs, solve_seg_len; // split-K segments of the X = G'^-1 r stream (fit.cu)
   int sm_count;

@@ -337,7 +337,7 @@ extern "C" mod_status mod_plan_create(const mod_layout* layout, const mod_config
   MOD_REQUIRE(cfg->select_mode >= 0 && cfg->select_mode <= 2, MOD_ERR_USAGE, "select_mode=%d invalid", cfg->select_mode);
   MOD_REQUIRE(cfg->stat_mode == MOD_STAT_POOLED, MOD_ERR_UNSUPPORTED, "stat_mode=%d not supported", cfg->stat_mode);
   MOD_REQUIRE(cfg->softmax_scale >= 0.f, MOD_ERR_INPUT, "softmax_scale=%g must be >= 0", cfg->softmax_scale);
-  MOD_REQUIRE(cfg->attn_kernel >= MOD_ATTN_DEFAULT && cfg->attn_kernel <= MOD_ATTN_PERSIST, MOD_ERR_USAGE,
+  MOD_REQUIRE(cfg->attn_kernel >= MOD_ATTN_DEFAULT && cfg->attn_kernel <= MOD_ATTN_WIDE, MOD_ERR_USAGE,
               "attn_kernel=%d invalid", cfg->attn_kernel);
 
   int ndev = 0;
@@ -581,7 +581,6 @@ extern "C" mod_status mod_plan_create(const mod_layout* layout, const mod_config
     P->solve_segs = (p + P->solve_seg_len - 1) / P->solve_seg_len;
   }
   P->ws_solve = off; off = align_up(off + (size_t)P->solve_segs * BH * (size_t)p * sizeof(double));
-  P->ws_sched = off; off = align_up(off + 16);   // K4 persistent schedule: item counter (attn.cu)
   P->ws_bytes = off;
   cudaSetDevice(prev_dev);
   P->create_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();

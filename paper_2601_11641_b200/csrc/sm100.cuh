@@ -49,19 +49,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-// one non-blocking test of a phase (true once the phase with the given parity has completed)
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n.reg .pred P1;\n"
-      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
-      "selp.u32 %0, 1, 0, P1;\n}\n"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-
 // try_wait with a suspend-time hint: the waiting warp sleeps until the phase completes (or the hint
 // expires) instead of re-issuing try_wait, so it leaves its sub-partition's issue slots to the others
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {

@@ -14,7 +14,7 @@ import paper_2601_11641_b200 as M
 
 TOPK = {"cogvideox-5b": 12, "wan2.1-14b-720p": 96, "hunyuanvideo-720p": 164}
 cfgs = (sys.argv[1] if len(sys.argv) > 1 else "cogvideox-5b,hunyuanvideo-720p").split(",")
-kerns = (sys.argv[2] if len(sys.argv) > 2 else "default,wide,persist").split(",")
+kerns = (sys.argv[2] if len(sys.argv) > 2 else "default,wide").split(",")
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 10
 dense = os.environ.get("DENSE", "0") == "1"
 

@@ -16,7 +16,7 @@ import synthetic as syn
 import paper_2601_11641_b200 as M
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "cogvideox-5b"
-kerns = (sys.argv[2] if len(sys.argv) > 2 else "default,wide,persist").split(",")
+kerns = (sys.argv[2] if len(sys.argv) > 2 else "default,wide").split(",")
 Ls = [int(x) for x in (sys.argv[3] if len(sys.argv) > 3 else "2,4,8,17,32,64").split(",")]
 w = syn.CONFIGS[cfg]
 REPS = int(os.environ.get("REPS", "10"))
