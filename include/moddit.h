@@ -162,12 +162,6 @@ const char* mod_attn_kernel_name(mod_plan plan);
 mod_status mod_collect_block_stats(mod_plan plan, const void* q, const void* k, float* stats, void* ws,
                                    void* stream);
 
-/* K1 at a re-estimation step t_p, after mod_block_sparse_attn_fwd_pool on the SAME q, k and the same ws
- * (Alg. 1: the fresh statistic is taken on the step's own Q, K): the same W as
- * mod_collect_block_stats, from the block means that call left in ws (its sums may differ in the last fp32
- * bits: another summation order).  stats: out fp32 [B,H,n,n]. */
-mod_status mod_collect_block_stats_pooled(mod_plan plan, float* stats, void* ws, void* stream);
-
 /* K2a: X = G^-1 M^T vec(U) per head, U = stats (fp32 [B,H,n,n]); x: out fp64 [B,H,p];
  * nae: nullable out fp32 [B,H] = ||U - MX||_F / ||U||_F (§4.2). */
 mod_status mod_fit_mixture(mod_plan plan, const float* stats, double* x, float* nae, void* ws, void* stream);
@@ -197,15 +191,6 @@ mod_status mod_update_online_mask(mod_plan plan, const float* stats_fresh, const
 mod_status mod_block_sparse_attn_fwd(mod_plan plan, const void* q, const void* k, const void* v,
                                      const int32_t* row_ptr, const int32_t* col_idx, void* o, float* lse,
                                      void* ws, void* stream);
-
-/* K4 + K1's first stage at a re-estimation step: the same O, lse as mod_block_sparse_attn_fwd, and the
- * block means qbar_i, kbar_i of q, k (north_star (1), reading Z1) left in ws (required) for
- * mod_collect_block_stats_pooled.  The default schedule computes the means from the Q tile it holds and
- * one extra K_i tile per query block (no separate pass over Q, K in HBM); the other schedules run K1's
- * pool kernel after the attention. */
-mod_status mod_block_sparse_attn_fwd_pool(mod_plan plan, const void* q, const void* k, const void* v,
-                                          const int32_t* row_ptr, const int32_t* col_idx, void* o, float* lse,
-                                          void* ws, void* stream);
 
 /* EXACT statistic (Eq. 2) in informativeness polarity (reading Z3):
  * for every block (i,j) listed in the CSR, stats[b,h,i,j] = -S_ij with

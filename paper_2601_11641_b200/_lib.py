@@ -63,13 +63,11 @@ SIGNATURES = {
     "mod_version": (C.c_char_p, []),
     "mod_attn_kernel_name": (C.c_char_p, [P]),
     "mod_collect_block_stats": (I32, [P, P, P, P, P, P]),
-    "mod_collect_block_stats_pooled": (I32, [P, P, P, P]),
     "mod_fit_mixture": (I32, [P, P, P, P, P, P]),
     "mod_keep_frames": (I32, [P, P, P, P, P]),
     "mod_predict_block_mask": (I32, [P, P, P, I32, I32, I32, P, C.POINTER(ModSelection), P, P, P, P]),
     "mod_update_online_mask": (I32, [P, P, P, P, P, P, P, P, P]),
     "mod_block_sparse_attn_fwd": (I32, [P, P, P, P, P, P, P, P, P, P]),
-    "mod_block_sparse_attn_fwd_pool": (I32, [P, P, P, P, P, P, P, P, P, P]),
     "mod_fill_dense_mask": (I32, [P, P, P, P]),
     "mod_collect_exact_sparsity": (I32, [P, P, P, P, P, P, C.c_float, P, P, P]),
     "mod_quant_buffer_bytes": (C.c_size_t, [P]),

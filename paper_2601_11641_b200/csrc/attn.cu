@@ -389,7 +389,7 @@ __device__ __forceinline__ void k4_commit(uint64_t* bar) {
   if constexpr (K4_LANE0_ISSUE) mma_commit(bar);
   else mma_commit_e(bar);
 }
-template <int D, int BN, bool POOL = false>
+template <int D, int BN>
 struct Attn1Cfg {
   static constexpr int BM = 128;
   static constexpr int NS = (512 - D) / BN > 7 ? 7 : (512 - D) / BN;
@@ -401,10 +401,9 @@ struct Attn1Cfg {
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + Q_BYTES;
   static constexpr int OFF_V = OFF_K + NS * KV_BYTES;
-  static constexpr int OFF_KI = OFF_V + VSTAGES * KV_BYTES;   // POOL: the query block's own K rows
-  static constexpr int OFF_BAR = OFF_KI + (POOL ? KV_BYTES : 0);
-  // q_full, k_full[NS], v_full[2], s_full[NS], p_full[NS], o_done[NS] (PV_j commits to o_done[j % NS]), ki_full
-  static constexpr int NUM_BARS = 1 + NS + VSTAGES + NS + NS + NS + 1;
+  static constexpr int OFF_BAR = OFF_V + VSTAGES * KV_BYTES;
+  // q_full, k_full[NS], v_full[2], s_full[NS], p_full[NS], o_done[NS] (PV_j commits to o_done[j % NS])
+  static constexpr int NUM_BARS = 1 + NS + VSTAGES + NS + NS + NS;
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr int TMEM_O = NS * BN;
   static constexpr uint32_t TMEM_COLS = (NS * BN + D) <= 256 ? 256 : 512;
@@ -416,9 +415,7 @@ struct Attn1Cfg {
   // per block; S on two alternating warps; pairs of MMAs paced by commits; four issuers over N-halves
   // with the left S half in the load warp: its waits delay the V loads, 2304 cycles per block.)
   static constexpr int S_WARP = 2 + SOFTMAX_WARPS;
-  static constexpr int POOL_WARP = S_WARP + 1;        // POOL: block means of Q_i and K_i (SM sub-partition 3)
-  static constexpr int THREADS = 64 + 32 * SOFTMAX_WARPS + 32 + (POOL ? 32 : 0);
-  static_assert(SMEM <= 232448, "Attn1Cfg: shared memory");
+  static constexpr int THREADS = 64 + 32 * SOFTMAX_WARPS + 32;
   static constexpr uint32_t IDESC_S = idesc_bf16_f32(BM, BN, false, false);
   static constexpr uint32_t IDESC_O = idesc_bf16_f32(BM, D, false, true);
 #ifndef K4_EMU
@@ -493,44 +490,13 @@ __device__ __forceinline__ float row_max(const float* s) {   // max of s[0..NC),
   return fmaxf(a, b);
 }
 
-// Block mean of one 128B-swizzled tile of `rows` token rows x D bf16 in shared memory (TMA layout: 64-column
-// atoms `box` bytes apart, row r's 16-byte chunk c at r*128 + ((c ^ (r & 7)) << 4); rows past the sequence
-// are the TMA's zero fill): lane l sums the column pair (2l, 2l+1) of every atom over rows [0, rows) in fp32
-// and writes mean = sum * inv to dst[64a + 2l, +2).  One warp; no barrier.
-template <int NATOM>
-__device__ __forceinline__ void pool_tile(const unsigned char* base, int box, int rows, float inv, float* dst, int lane) {
-#pragma unroll 1
-  for (int a = 0; a < NATOM; ++a) {
-    const unsigned char* atom = base + a * box + (lane & 3) * 4;
-    auto word = [&](int r) {   // bf16 pair (2l, 2l+1) of row r as float2
-      const uint32_t w = *reinterpret_cast<const uint32_t*>(atom + r * 128 + ((((lane >> 2) ^ (r & 7))) << 4));
-      return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
-    };
-    float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-    int r = 0;
-#pragma unroll 1
-    for (; r + 4 <= rows; r += 4) {
-#pragma unroll
-      for (int u = 0; u < 4; ++u) acc[u] = fadd2(acc[u], word(r + u));
-    }
-#pragma unroll 1
-    for (; r < rows; ++r) acc[0] = fadd2(acc[0], word(r));
-    const float2 t = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
-    *reinterpret_cast<float2*>(dst + a * 64 + 2 * lane) = make_float2(t.x * inv, t.y * inv);
-  }
-}
-
-// POOL = true (mod_block_sparse_attn_fwd_pool, the re-estimation step t_p where K1 follows K4 on the same
-// Q, K): the CTA of query block i also loads K_i (the keys of block i) and one more warp writes the block
-// means qbar_i, kbar_i of K1 (stats.cu pool_kernel's output) from the Q tile and the K_i tile in shared
-// memory, so K1's HBM pass over Q and K disappears.  The attention part is unchanged (same O, lse bits).
-template <int D, int BN, bool POOL>
-__global__ void __launch_bounds__(Attn1Cfg<D, BN, POOL>::THREADS, 1)
+template <int D, int BN>
+__global__ void __launch_bounds__(Attn1Cfg<D, BN>::THREADS, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const int* __restrict__ row_ptr,
                     const int* __restrict__ col_idx, __nv_bfloat16* __restrict__ out, float* __restrict__ lse,
-                    int N, int n, int block, float scale_log2, float* __restrict__ qbar, float* __restrict__ kbar) {
-  using C = Attn1Cfg<D, BN, POOL>;
+                    int N, int n, int block, float scale_log2) {
+  using C = Attn1Cfg<D, BN>;
   constexpr int NS = C::NS;
   extern __shared__ __align__(1024) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
@@ -540,8 +506,7 @@ __global__ void __launch_bounds__(Attn1Cfg<D, BN, POOL>::THREADS, 1)
   uint64_t* s_full = v_full + C::VSTAGES;
   uint64_t* p_full = s_full + NS;
   uint64_t* o_done = p_full + NS;
-  uint64_t* ki_full = o_done + NS;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ki_full + 1);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + NS);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0 && (smem_u32(smem) & 1023u) != 0) __trap();   // SWIZZLE_128B needs 1024B alignment
@@ -553,7 +518,6 @@ __global__ void __launch_bounds__(Attn1Cfg<D, BN, POOL>::THREADS, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
-    mbar_init(ki_full, 1);
     for (int s = 0; s < NS; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&s_full[s], 1);
@@ -629,7 +593,7 @@ __global__ void __launch_bounds__(Attn1Cfg<D, BN, POOL>::THREADS, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0 && (L > 0 || POOL)) {
+    if (lane == 0 && L > 0) {
       tma_prefetch_desc(&tm_q);
       tma_prefetch_desc(&tm_k);
       tma_prefetch_desc(&tm_v);
@@ -637,12 +601,6 @@ __global__ void __launch_bounds__(Attn1Cfg<D, BN, POOL>::THREADS, 1)
 #pragma unroll
       for (int a = 0; a < C::NATOM; ++a)
         tma_load_3d(smem + C::OFF_Q + a * C::Q_BOX, &tm_q, q_full, a * 64, qi * block, bh, pol_q);
-      if constexpr (POOL) {   // K_i for the block mean (also for an empty list)
-        mbar_arrive_expect_tx(ki_full, C::KV_BYTES);
-#pragma unroll
-        for (int a = 0; a < C::NATOM; ++a)
-          tma_load_3d(smem + C::OFF_KI + a * C::KV_BOX, &tm_k, ki_full, a * 64, qi * block, bh, pol_kv);
-      }
       // demand order of the MMA warps: K_0 .. K_{NS-1}, then V_j, K_{j+NS} for j = 0, 1, ...
       for (int j = 0; j < NS && j < L; ++j) load_k(j);
       for (int j = 0; j < L; ++j) {
@@ -685,15 +643,6 @@ __global__ void __launch_bounds__(Attn1Cfg<D, BN, POOL>::THREADS, 1)
         }
       }
     }
-  } else if (POOL && warp == C::POOL_WARP) {
-    // ------------------------------------------------------------ K1 block means of Q_i and K_i
-    const int rows = min(block, N - qi * block);
-    const float inv = 1.0f / (float)rows;
-    const size_t o = ((size_t)bh * n + qi) * D;
-    mbar_wait(q_full, 0);
-    pool_tile<C::NATOM>(smem + C::OFF_Q, C::Q_BOX, rows, inv, qbar + o, lane);
-    mbar_wait(ki_full, 0);
-    pool_tile<C::NATOM>(smem + C::OFF_KI, C::KV_BOX, rows, inv, kbar + o, lane);
   } else if (warp < 2 + C::SOFTMAX_WARPS) {
     // ------------------------------------------------------------ softmax / epilogue (8 independent warps)
     constexpr int COLS = C::COLS, OCOLS = C::OCOLS, OCH = OCOLS < 32 ? OCOLS : 32;
@@ -1500,29 +1449,10 @@ mod_status launch_rows(mod_plan P, Kern kern, int D, int BN, const void* q, cons
   return MOD_OK;
 }
 
-// The default schedule; with qbar / kbar (POOL) the same launch also leaves K1's block means in them.
 template <int D, int BN>
 mod_status launch_default(mod_plan P, const void* q, const void* k, const void* v, const int* row_ptr,
-                          const int* col_idx, void* o, float* lse, cudaStream_t s, float* qbar = nullptr,
-                          float* kbar = nullptr) {
-  const int BH = P->L.batch * P->L.heads;
-  CUtensorMap tq, tk, tv;
-  mod_status st;
-  if ((st = make_map(&tq, q, BH, P->N, D, 128)) != MOD_OK) return st;
-  if ((st = make_map(&tk, k, BH, P->N, D, BN)) != MOD_OK) return st;
-  if ((st = make_map(&tv, v, BH, P->N, D, BN)) != MOD_OK) return st;
-  const float scale_log2 = P->scale * 1.4426950408889634f;
-  auto go = [&](auto pc) -> mod_status {
-    constexpr bool POOL = decltype(pc)::value;
-    using Cfg = Attn1Cfg<D, BN, POOL>;
-    auto kern = attn_fwd_kernel<D, BN, POOL>;
-    MOD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-    kern<<<BH * P->n, Cfg::THREADS, Cfg::SMEM, s>>>(tq, tk, tv, row_ptr, col_idx, (__nv_bfloat16*)o, lse, P->N, P->n,
-                                                    P->L.block, scale_log2, qbar, kbar);
-    MOD_LAUNCH_CHECK();
-    return MOD_OK;
-  };
-  return qbar ? go(std::true_type{}) : go(std::false_type{});
+                          const int* col_idx, void* o, float* lse, cudaStream_t s) {
+  return launch_rows<Attn1Cfg<D, BN>>(P, attn_fwd_kernel<D, BN>, D, BN, q, k, v, row_ptr, col_idx, o, lse, s);
 }
 
 template <int D, int BN>
@@ -1603,16 +1533,19 @@ extern "C" const char* mod_attn_kernel_name(mod_plan P) {
   }
 }
 
-// The launch of the plan's schedule.  qbar / kbar non-NULL: also K1's block means (fused into the default
-// schedule; the other schedules are followed by K1's pool kernel).  *launches counts the kernels.
-static mod_status attn_dispatch(mod_plan P, const void* q, const void* k, const void* v, const int32_t* row_ptr,
-                                const int32_t* col_idx, void* o, float* lse, cudaStream_t s, float* qbar, float* kbar,
-                                int* launches) {
+extern "C" mod_status mod_block_sparse_attn_fwd(mod_plan P, const void* q, const void* k, const void* v,
+                                                const int32_t* row_ptr, const int32_t* col_idx, void* o, float* lse,
+                                                void* ws, void* stream) {
+  MOD_NVTX("mod_block_sparse_attn_fwd");
+  (void)ws;
+  mod_status st = mod_validate_plan(P);
+  if (st != MOD_OK) return st;
+  MOD_REQUIRE(q && k && v && row_ptr && col_idx && o, MOD_ERR_USAGE,
+              "mod_block_sparse_attn_fwd: q, k, v, row_ptr, col_idx, o must be non-NULL");
+  MOD_REQUIRE(((uintptr_t)o & 15) == 0, MOD_ERR_INPUT, "o must be 16-byte aligned");
+  cudaStream_t s = as_stream(stream);
   const int D = P->L.head_dim, BN = P->L.block;
-  mod_status st;
-  *launches = 1;
-  const int kern = effective_kernel(P);
-  switch (kern) {
+  switch (effective_kernel(P)) {
     case MOD_ATTN_PAIR:
       st = D == 128 ? launch_pair<128>(P, q, k, v, row_ptr, col_idx, o, lse, s)
                     : launch_pair<64>(P, q, k, v, row_ptr, col_idx, o, lse, s);
@@ -1628,53 +1561,11 @@ static mod_status attn_dispatch(mod_plan P, const void* q, const void* k, const 
       else st = launch_split<64, 64>(P, q, k, v, row_ptr, col_idx, o, lse, s);
       break;
     default:
-      if (D == 128 && BN == 128) st = launch_default<128, 128>(P, q, k, v, row_ptr, col_idx, o, lse, s, qbar, kbar);
-      else if (D == 64 && BN == 128) st = launch_default<64, 128>(P, q, k, v, row_ptr, col_idx, o, lse, s, qbar, kbar);
-      else if (D == 128 && BN == 64) st = launch_default<128, 64>(P, q, k, v, row_ptr, col_idx, o, lse, s, qbar, kbar);
-      else st = launch_default<64, 64>(P, q, k, v, row_ptr, col_idx, o, lse, s, qbar, kbar);
-      return st;
+      if (D == 128 && BN == 128) st = launch_default<128, 128>(P, q, k, v, row_ptr, col_idx, o, lse, s);
+      else if (D == 64 && BN == 128) st = launch_default<64, 128>(P, q, k, v, row_ptr, col_idx, o, lse, s);
+      else if (D == 128 && BN == 64) st = launch_default<128, 64>(P, q, k, v, row_ptr, col_idx, o, lse, s);
+      else st = launch_default<64, 64>(P, q, k, v, row_ptr, col_idx, o, lse, s);
   }
-  if (st == MOD_OK && qbar) {
-    st = mod_launch_pool_means(P, q, k, qbar, kbar, s);
-    *launches = 2;
-  }
-  return st;
-}
-
-static mod_status attn_check(mod_plan P, const void* q, const void* k, const void* v, const int32_t* row_ptr,
-                             const int32_t* col_idx, void* o, const char* who) {
-  mod_status st = mod_validate_plan(P);
-  if (st != MOD_OK) return st;
-  MOD_REQUIRE(q && k && v && row_ptr && col_idx && o, MOD_ERR_USAGE, "%s: q, k, v, row_ptr, col_idx, o must be non-NULL",
-              who);
-  MOD_REQUIRE(((uintptr_t)o & 15) == 0, MOD_ERR_INPUT, "o must be 16-byte aligned");
-  return MOD_OK;
-}
-
-extern "C" mod_status mod_block_sparse_attn_fwd(mod_plan P, const void* q, const void* k, const void* v,
-                                                const int32_t* row_ptr, const int32_t* col_idx, void* o, float* lse,
-                                                void* ws, void* stream) {
-  MOD_NVTX("mod_block_sparse_attn_fwd");
-  (void)ws;
-  mod_status st = attn_check(P, q, k, v, row_ptr, col_idx, o, "mod_block_sparse_attn_fwd");
-  if (st != MOD_OK) return st;
-  int launches = 0;
-  st = attn_dispatch(P, q, k, v, row_ptr, col_idx, o, lse, as_stream(stream), nullptr, nullptr, &launches);
-  if (st == MOD_OK) mod_note_launches(launches);
-  return st;
-}
-
-extern "C" mod_status mod_block_sparse_attn_fwd_pool(mod_plan P, const void* q, const void* k, const void* v,
-                                                     const int32_t* row_ptr, const int32_t* col_idx, void* o,
-                                                     float* lse, void* ws, void* stream) {
-  MOD_NVTX("mod_block_sparse_attn_fwd_pool");
-  mod_status st = attn_check(P, q, k, v, row_ptr, col_idx, o, "mod_block_sparse_attn_fwd_pool");
-  if (st != MOD_OK) return st;
-  MOD_REQUIRE(ws, MOD_ERR_USAGE, "mod_block_sparse_attn_fwd_pool: ws must be non-NULL (it receives the block means)");
-  float* qbar = reinterpret_cast<float*>(static_cast<char*>(ws) + P->ws_qbar);
-  float* kbar = reinterpret_cast<float*>(static_cast<char*>(ws) + P->ws_kbar);
-  int launches = 0;
-  st = attn_dispatch(P, q, k, v, row_ptr, col_idx, o, lse, as_stream(stream), qbar, kbar, &launches);
-  if (st == MOD_OK) mod_note_launches(launches);
+  if (st == MOD_OK) mod_note_launches(1);
   return st;
 }

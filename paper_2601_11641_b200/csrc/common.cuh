@@ -70,8 +70,6 @@ struct mod_plan_s {
 };
 
 mod_status mod_validate_plan(mod_plan plan);
-// K1's pool stage (stats.cu): block means of Q and K, fp32 [BH, n, D]
-mod_status mod_launch_pool_means(mod_plan P, const void* q, const void* k, float* qbar, float* kbar, cudaStream_t s);
 
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 

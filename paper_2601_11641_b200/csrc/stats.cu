@@ -331,31 +331,27 @@ __global__ void __launch_bounds__(Score2Cfg<D>::THREADS, 1) score_kernel(
 
 }  // namespace
 
-// K1's first stage: the block means of Q and K into qbar / kbar (fp32 [BH, n, D]).
-mod_status mod_launch_pool_means(mod_plan P, const void* q, const void* k, float* qbar, float* kbar, cudaStream_t s) {
-  const int BH = P->L.batch * P->L.heads, n = P->n;
-  const dim3 pg(n, BH, 2);
-  if (P->L.head_dim == 128)
-    pool_kernel<128><<<pg, 256, 0, s>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k, qbar, kbar, P->N, n, P->L.block);
-  else
-    pool_kernel<64><<<pg, 256, 0, s>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k, qbar, kbar, P->N, n, P->L.block);
-  MOD_LAUNCH_CHECK();
-  return MOD_OK;
-}
-
-// K1's score stage from the block means in ws: the bf16 hi/lo split, then the two tcgen05 score passes.
-static mod_status score_from_means(mod_plan P, float* stats, void* ws, cudaStream_t s) {
+extern "C" mod_status mod_collect_block_stats(mod_plan P, const void* q, const void* k, float* stats, void* ws,
+                                              void* stream) {
+  MOD_NVTX("mod_collect_block_stats");
+  mod_status st = mod_validate_plan(P);
+  if (st != MOD_OK) return st;
+  MOD_REQUIRE(q && k && stats && ws, MOD_ERR_USAGE, "mod_collect_block_stats: q, k, stats, ws must be non-NULL");
   const int BH = P->L.batch * P->L.heads, n = P->n, D = P->L.head_dim;
   const int T = (n + 127) / 128, NCH = (n + Score2Cfg<128>::CHUNK_COLS - 1) / Score2Cfg<128>::CHUNK_COLS;
   float* qbar = reinterpret_cast<float*>(static_cast<char*>(ws) + P->ws_qbar);   // fp32 means [BH, n, D]
   float* kbar = reinterpret_cast<float*>(static_cast<char*>(ws) + P->ws_kbar);
   unsigned char* qs = static_cast<unsigned char*>(ws) + P->ws_qs;                  // pre-split tiles [BH][T][hi|lo]
   unsigned char* ks = static_cast<unsigned char*>(ws) + P->ws_ks;
+  cudaStream_t s = as_stream(stream);
+  const dim3 pg(n, BH, 2);
   const dim3 sg(T, NCH, BH);
   float2* part = reinterpret_cast<float2*>(static_cast<char*>(ws) + P->ws_part);   // [BH, n, NCH] (free during K1)
   auto run = [&](auto dc) -> mod_status {
     constexpr int DD = decltype(dc)::value;
     using C = Score2Cfg<DD>;
+    pool_kernel<DD><<<pg, 256, 0, s>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k, qbar, kbar, P->N, n, P->L.block);
+    MOD_LAUNCH_CHECK();
     const size_t chunks = 2ull * BH * T * 128 * (DD / 8);
     split_kernel<DD><<<(unsigned)((chunks + 255) / 256), 256, 0, s>>>(qbar, kbar, qs, ks, n, T, BH);
     MOD_LAUNCH_CHECK();
@@ -367,30 +363,8 @@ static mod_status score_from_means(mod_plan P, float* stats, void* ws, cudaStrea
     MOD_LAUNCH_CHECK();
     return MOD_OK;
   };
-  return D == 128 ? run(std::integral_constant<int, 128>{}) : run(std::integral_constant<int, 64>{});
-}
-
-extern "C" mod_status mod_collect_block_stats(mod_plan P, const void* q, const void* k, float* stats, void* ws,
-                                              void* stream) {
-  MOD_NVTX("mod_collect_block_stats");
-  mod_status st = mod_validate_plan(P);
+  st = D == 128 ? run(std::integral_constant<int, 128>{}) : run(std::integral_constant<int, 64>{});
   if (st != MOD_OK) return st;
-  MOD_REQUIRE(q && k && stats && ws, MOD_ERR_USAGE, "mod_collect_block_stats: q, k, stats, ws must be non-NULL");
-  cudaStream_t s = as_stream(stream);
-  float* qbar = reinterpret_cast<float*>(static_cast<char*>(ws) + P->ws_qbar);
-  float* kbar = reinterpret_cast<float*>(static_cast<char*>(ws) + P->ws_kbar);
-  if ((st = mod_launch_pool_means(P, q, k, qbar, kbar, s)) != MOD_OK) return st;
-  if ((st = score_from_means(P, stats, ws, s)) != MOD_OK) return st;
   mod_note_launches(4);
-  return MOD_OK;
-}
-
-extern "C" mod_status mod_collect_block_stats_pooled(mod_plan P, float* stats, void* ws, void* stream) {
-  MOD_NVTX("mod_collect_block_stats_pooled");
-  mod_status st = mod_validate_plan(P);
-  if (st != MOD_OK) return st;
-  MOD_REQUIRE(stats && ws, MOD_ERR_USAGE, "mod_collect_block_stats_pooled: stats, ws must be non-NULL");
-  if ((st = score_from_means(P, stats, ws, as_stream(stream))) != MOD_OK) return st;
-  mod_note_launches(3);
   return MOD_OK;
 }

@@ -185,15 +185,6 @@ class Plan:
         return out
 
     @_on_device
-    def collect_block_stats_pooled(self, out=None):
-        """K1 from the block means the last ``block_sparse_attn_fwd(..., pool=True)`` left in this plan's
-        workspace (the re-estimation step's Q, K; include/moddit.h mod_collect_block_stats_pooled)."""
-        out = self.empty_stats() if out is None else out
-        self._check_stats("out", out)
-        check(lib.mod_collect_block_stats_pooled(self._h, _ptr(out), _ptr(self.workspace()), _stream()))
-        return out
-
-    @_on_device
     def fit_mixture(self, stats, out=None, want_nae: bool = False):
         self._check_stats("stats", stats)
         out = self.empty_x() if out is None else out
@@ -240,10 +231,7 @@ class Plan:
                                          _ptr(x_prev), _ptr(x_curr), _ptr(self.workspace()), _stream()))
 
     @_on_device
-    def block_sparse_attn_fwd(self, q, k, v, row_ptr, col_idx, out=None, lse=None, want_lse: bool = True,
-                              pool: bool = False):
-        """K4 (Eq. 1 over the index lists).  pool=True: also K1's block means of q, k into the workspace,
-        for collect_block_stats_pooled (mod_block_sparse_attn_fwd_pool)."""
+    def block_sparse_attn_fwd(self, q, k, v, row_ptr, col_idx, out=None, lse=None, want_lse: bool = True):
         self._check_qkv(q, k, v)
         self._check_csr(row_ptr, col_idx)
         out = torch.empty_like(q) if out is None else out
@@ -251,9 +239,8 @@ class Plan:
         if lse is None and want_lse:
             lse = torch.empty(q.shape[:-1], dtype=torch.float32, device=q.device)
         self._check("lse", lse, torch.float32, tuple(q.shape[:-1]), optional=True)
-        fn = lib.mod_block_sparse_attn_fwd_pool if pool else lib.mod_block_sparse_attn_fwd
-        check(fn(self._h, _ptr(q), _ptr(k), _ptr(v), _ptr(row_ptr), _ptr(col_idx), _ptr(out), _ptr(lse),
-                 _ptr(self.workspace()), _stream()))
+        check(lib.mod_block_sparse_attn_fwd(self._h, _ptr(q), _ptr(k), _ptr(v), _ptr(row_ptr), _ptr(col_idx),
+                                            _ptr(out), _ptr(lse), _ptr(self.workspace()), _stream()))
         return out, lse
 
     @_on_device
