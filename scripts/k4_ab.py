@@ -42,7 +42,8 @@ for cfg in cfgs:
         flops += float((sizes[rows] * sizes[cols]).sum()) * 4 * D
     nnz = float(rp[..., -1].sum())
     ref = None
-    for kern in kerns:
+    for kspec in kerns:
+        kern, pool = kspec.split("+")[0], kspec.endswith("+pool")   # "default+pool": K4 with K1's fused means
         P = M.Plan(w, top_k=1, attn_kernel=kern)
         o, lse = P.block_sparse_attn_fwd(q, k, v, rp, ci)
         torch.cuda.synchronize()
@@ -52,17 +53,17 @@ for cfg in cfgs:
         else:
             dev = (o.float() - ref).abs().max().item()
         for _ in range(2):
-            P.block_sparse_attn_fwd(q, k, v, rp, ci, out=o, lse=lse)
+            P.block_sparse_attn_fwd(q, k, v, rp, ci, out=o, lse=lse, pool=pool)
         st = torch.cuda.current_stream()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         e0.record(st)
         for _ in range(reps):
-            P.block_sparse_attn_fwd(q, k, v, rp, ci, out=o, lse=lse)
+            P.block_sparse_attn_fwd(q, k, v, rp, ci, out=o, lse=lse, pool=pool)
         e1.record(st)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / reps
-        print(json.dumps({"config": cfg, "kernel": P.attn_kernel_name(), "ms": round(ms, 4),
+        print(json.dumps({"config": cfg, "kernel": P.attn_kernel_name() + ("+pool" if pool else ""), "ms": round(ms, 4),
                           "tflops": round(flops / ms / 1e9, 1), "nnz": nnz,
                           "sparsity": round(1 - nnz / (rp.shape[0] * rp.shape[1] * n * n), 4),
                           "max_dev_vs_first": dev}), flush=True)
