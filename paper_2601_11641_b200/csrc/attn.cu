@@ -374,6 +374,22 @@ __global__ void __launch_bounds__(320, 1)
 #ifndef K4_LANE0_ISSUE
 #define K4_LANE0_ISSUE 1
 #endif
+// Q of the query block one wave ahead (item + number of SMs: the CTA the block scheduler starts about when
+// this one ends) is prefetched into L2 by the producer, so that CTA's first load -- the only HBM read on its
+// critical path (K / V of the head are L2-resident) -- hits L2.
+#ifndef K4_PREFETCH_Q
+#define K4_PREFETCH_Q 1
+#endif
+template <int NATOM>
+__device__ __forceinline__ void prefetch_next_q(const CUtensorMap* tm_q, int item, int n, int block) {
+  if constexpr (K4_PREFETCH_Q) {
+    const int nx = item + (int)num_sms();
+    if (nx < (int)gridDim.x) {
+#pragma unroll
+      for (int a = 0; a < NATOM; ++a) tma_prefetch_l2_3d(tm_q, a * 64, (nx % n) * block, nx / n);
+    }
+  }
+}
 
 template <uint32_t A_OFF, uint32_t B_OFF>
 __device__ __forceinline__ void k4_mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
@@ -603,6 +619,7 @@ __global__ void __launch_bounds__(Attn1Cfg<D, BN>::THREADS, 1)
         tma_load_3d(smem + C::OFF_Q + a * C::Q_BOX, &tm_q, q_full, a * 64, qi * block, bh, pol_q);
       // demand order of the MMA warps: K_0 .. K_{NS-1}, then V_j, K_{j+NS} for j = 0, 1, ...
       for (int j = 0; j < NS && j < L; ++j) load_k(j);
+      prefetch_next_q<C::NATOM>(&tm_q, item, n, block);
       for (int j = 0; j < L; ++j) {
         if (j >= 2) K4_WAIT(&o_done[(j - 2) % NS], ((j - 2) / NS) & 1);   // PV_{j-2} has consumed V slot j % 2
         load_v(j);
@@ -923,6 +940,7 @@ __global__ void __launch_bounds__(WideCfg<D, BN>::THREADS, 1)
       for (int a = 0; a < C::NATOM; ++a)
         tma_load_3d(smem + C::OFF_Q + a * C::Q_BOX, &tm_q, q_full, a * 64, qi * block, bh, pol_q);
       for (int j = 0; j < NS && j < L; ++j) load_k(j);
+      prefetch_next_q<C::NATOM>(&tm_q, item, n, block);
       for (int j = 0; j < L; ++j) {
         if (j >= 2) K4_WAIT(&o_done[(j - 2) % NS], ((j - 2) / NS) & 1);
         load_v(j);
