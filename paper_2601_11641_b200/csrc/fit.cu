@@ -22,41 +22,14 @@ using namespace sm100;
 
 namespace {
 
-// Compensated fp32 accumulation (Knuth's TwoSum): s + e carries the running sum of fp32 terms without
-// rounding error beyond (k u)^2 relative for k terms (non-negative maps); two independent chains are
-// packed in one float2 so every step is FADD2s on the FMA pipe (no fp32 -> fp64 conversions in the
-// loops).  The chains are converted to fp64 and added once per partial sum.
-struct Acc2 {
-  float2 s = make_float2(0.f, 0.f), e = make_float2(0.f, 0.f);
-  __device__ __forceinline__ void add(float2 x) {
-    const float2 t = fadd2(s, x);
-    const float2 bp = fadd2(t, make_float2(-s.x, -s.y));                      // t - s
-    const float2 ap = fadd2(t, make_float2(-bp.x, -bp.y));                    // t - bp
-    const float2 err = fadd2(fadd2(s, make_float2(-ap.x, -ap.y)),             // (s - ap) + (x - bp)
-                             fadd2(x, make_float2(-bp.x, -bp.y)));
-    e = fadd2(e, err);
-    s = t;
-  }
-  __device__ __forceinline__ double total() const {
-    return ((double)s.x + (double)e.x) + ((double)s.y + (double)e.y);
-  }
-};
-
 // One CTA per (head, tile of `rows` consecutive map rows).  The tile is a contiguous run of rows * n fp32
 // values of U: its 16-byte-aligned interior is staged in shared memory by ONE bulk copy on the TMA engine
 // (HBM-bound: every map byte is read once; two CTAs per SM overlap one's copy with the other's sums),
 // then the C (diagonal), D (column) and E (frame-square) partial sums of the tile are formed from shared
-// memory, each in a fixed order (deterministic) with compensated fp32 chains (Acc2).
-// MERGE (K3, Eq. 5): U is the history map; before the sums, every selected entry (i,j) of the
-// tile's rows is replaced, in shared memory and in U, by W[i,j] / sum_{j' selected} W[i,j'] (masked_renorm;
-// the fp64 row sum rounded once, as merge_kernel did) or W[i,j] -- the Eq. 5 merge fused into the fit's
-// single read of the map.
-template <bool MERGE>
-__global__ void __launch_bounds__(256) project_kernel(float* __restrict__ U, double* __restrict__ part,
+// memory in fp64, each in a fixed order (deterministic).
+__global__ void __launch_bounds__(256) project_kernel(const float* __restrict__ U, double* __restrict__ part,
                                                        const int* __restrict__ frame_ab, int n, int F, int p,
-                                                       int tiles, int rows, const float* __restrict__ W,
-                                                       const int* __restrict__ row_ptr,
-                                                       const int* __restrict__ col_idx, int renorm) {
+                                                       int tiles, int rows) {
   extern __shared__ __align__(128) float tile_raw[];
   __shared__ __align__(8) uint64_t bar;
   const size_t bh = blockIdx.y;
@@ -84,60 +57,47 @@ __global__ void __launch_bounds__(256) project_kernel(float* __restrict__ U, dou
   for (size_t e = head + 4 * nvec + threadIdx.x; e < count; e += blockDim.x) t[e] = src[e];
   if (bytes > 0) mbar_wait(&bar, 0);
   __syncthreads();
-  const int tid = threadIdx.x;
-  const int warp = tid / 32, lane = tid % 32;
-  if constexpr (MERGE) {
-    // one warp per row of the tile: the Eq. 5 merge of its selected entries
-    const int* rp = row_ptr + bh * (n + 1);
-    const int* ci = col_idx + bh * (size_t)n * n;
-    for (int i = warp; i < R; i += blockDim.x / 32) {
-      const int gi = i0 + i;
-      const float* Wr = W + (bh * n + gi) * (size_t)n;
-      float* Ur = U + (bh * n + gi) * (size_t)n;
-      const int beg = rp[gi], end = rp[gi + 1];
-      double sum = 0.0;
-      if (renorm) {
-        for (int e = beg + lane; e < end; e += 32) sum += (double)Wr[ci[e]];
-        sum = warp_sum_d(sum);
-      }
-      for (int e = beg + lane; e < end; e += 32) {
-        const int j = ci[e];
-        const float v = renorm ? (sum > 0.0 ? (float)((double)Wr[j] / sum) : 0.f) : Wr[j];
-        t[i * n + j] = v;
-        Ur[j] = v;
-      }
-    }
-    __syncthreads();
-  }
   double* out = part + (bh * tiles + tile) * (size_t)p;
-  // C part: diagonal offset d = k - (n-1); entries (i, i+d) of this tile, rows ilo.. in two interleaved
-  // chains (i even / odd)
+  const int tid = threadIdx.x;
+  // C part: diagonal offset d = k - (n-1); entries (i, i+d) of this tile
+  // (each sum is formed as four interleaved partial sums over i mod 4 added at the end: a fixed order,
+  // with four independent shared-memory load -> add chains in flight)
   for (int k = tid; k < 2 * n - 1; k += blockDim.x) {
     const int d = k - (n - 1);
     const int ilo = max(0, -(i0 + d)), ihi = min(R, n - (i0 + d));   // rows of the tile with 0 <= i0+i+d < n
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
     const float* q = t + i0 + d;   // q[i * (n + 1)] = t[i * n + i0 + i + d]
-    Acc2 a;
     int i = ilo;
-    for (; i + 2 <= ihi; i += 2) a.add(make_float2(q[i * (n + 1)], q[(i + 1) * (n + 1)]));
-    if (i < ihi) a.add(make_float2(q[i * (n + 1)], 0.f));
-    out[k] = a.total();
+    for (; i + 4 <= ihi; i += 4) {
+      s0 += (double)q[i * (n + 1)];
+      s1 += (double)q[(i + 1) * (n + 1)];
+      s2 += (double)q[(i + 2) * (n + 1)];
+      s3 += (double)q[(i + 3) * (n + 1)];
+    }
+    for (; i < ihi; ++i) s0 += (double)q[i * (n + 1)];
+    out[k] = (s0 + s1) + (s2 + s3);
   }
-  // D part: column sums of this tile (two interleaved chains over the rows)
+  // D part: column sums of this tile
   for (int j = tid; j < n; j += blockDim.x) {
-    Acc2 a;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
     int i = 0;
-    for (; i + 2 <= R; i += 2) a.add(make_float2(t[i * n + j], t[(i + 1) * n + j]));
-    if (i < R) a.add(make_float2(t[i * n + j], 0.f));
-    out[2 * n - 1 + j] = a.total();
+    for (; i + 4 <= R; i += 4) {
+      s0 += (double)t[i * n + j];
+      s1 += (double)t[(i + 1) * n + j];
+      s2 += (double)t[(i + 2) * n + j];
+      s3 += (double)t[(i + 3) * n + j];
+    }
+    for (; i < R; ++i) s0 += (double)t[i * n + j];
+    out[2 * n - 1 + j] = (s0 + s1) + (s2 + s3);
   }
   // E part: frame squares intersecting this tile (one warp per frame)
+  const int warp = tid / 32, lane = tid % 32;
   for (int r = warp; r < F; r += blockDim.x / 32) {
     const int a = frame_ab[2 * r], b = frame_ab[2 * r + 1];
-    Acc2 acc;
+    double s = 0.0;
     for (int i = max(a, i0); i <= min(b, i1 - 1); ++i)
-      for (int j = a + lane; j <= b; j += 64)
-        acc.add(make_float2(t[(i - i0) * n + j], j + 32 <= b ? t[(i - i0) * n + j + 32] : 0.f));
-    const double s = warp_sum_d(acc.total());
+      for (int j = a + lane; j <= b; j += 32) s += (double)t[(i - i0) * n + j];
+    s = warp_sum_d(s);
     if (lane == 0) out[3 * n - 1 + r] = s;
   }
 }
@@ -362,6 +322,30 @@ __global__ void keep_kernel(const double* __restrict__ xa, const double* __restr
 }
 
 // Eq. 5 merge; one warp per row
+__global__ void merge_kernel(const float* __restrict__ W, const int* __restrict__ row_ptr,
+                             const int* __restrict__ col_idx, float* __restrict__ hist, int n, int renorm) {
+  const size_t bh = blockIdx.y;
+  const int i = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (i >= n) return;
+  const int* rp = row_ptr + bh * (n + 1);
+  const int* ci = col_idx + bh * (size_t)n * n;
+  const float* Wr = W + (bh * n + i) * (size_t)n;
+  float* Hr = hist + (bh * n + i) * (size_t)n;
+  const int beg = rp[i], end = rp[i + 1];
+  if (!renorm) {
+    for (int e = beg + lane; e < end; e += 32) Hr[ci[e]] = Wr[ci[e]];
+    return;
+  }
+  double s = 0.0;
+  for (int e = beg + lane; e < end; e += 32) s += (double)Wr[ci[e]];
+  s = warp_sum_d(s);
+  for (int e = beg + lane; e < end; e += 32) {
+    const int j = ci[e];
+    Hr[j] = s > 0.0 ? (float)((double)Wr[j] / s) : 0.f;
+  }
+}
+
 __global__ void roll_kernel(double* __restrict__ x_prev, double* __restrict__ x_curr, const double* __restrict__ X,
                             size_t total) {
   const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -371,30 +355,13 @@ __global__ void roll_kernel(double* __restrict__ x_prev, double* __restrict__ x_
 }
 
 // r = M^T vec U for every head, then X = G'^{-1} r.  4 launches.
-// merge != NULL (K3): the Eq. 5 merge of the fresh map W into U (the history) happens inside the projection
-// (project_kernel<true>), which then writes the merged entries back to U.
-struct MergeArgs {
-  const float* W;
-  const int* row_ptr;
-  const int* col_idx;
-  int renorm;
-};
-mod_status fit_from_map(mod_plan P, const float* U, double* X, void* ws, cudaStream_t s,
-                        const MergeArgs* merge = nullptr) {
+mod_status fit_from_map(mod_plan P, const float* U, double* X, void* ws, cudaStream_t s) {
   const int BH = P->L.batch * P->L.heads, n = P->n, p = P->p, tiles = P->proj_tiles;
   double* part = reinterpret_cast<double*>(static_cast<char*>(ws) + P->ws_part);
   double* r = reinterpret_cast<double*>(static_cast<char*>(ws) + P->ws_r);
   const int smem = (P->proj_rows * n + 8) * (int)sizeof(float);
-  if (merge) {
-    MOD_CUDA(cudaFuncSetAttribute(project_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    project_kernel<true><<<dim3(tiles, BH), 256, smem, s>>>(const_cast<float*>(U), part, P->d_frame_ab, n, P->F, p,
-                                                            tiles, P->proj_rows, merge->W, merge->row_ptr,
-                                                            merge->col_idx, merge->renorm);
-  } else {
-    MOD_CUDA(cudaFuncSetAttribute(project_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    project_kernel<false><<<dim3(tiles, BH), 256, smem, s>>>(const_cast<float*>(U), part, P->d_frame_ab, n, P->F, p,
-                                                             tiles, P->proj_rows, nullptr, nullptr, nullptr, 0);
-  }
+  MOD_CUDA(cudaFuncSetAttribute(project_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  project_kernel<<<dim3(tiles, BH), 256, smem, s>>>(U, part, P->d_frame_ab, n, P->F, p, tiles, P->proj_rows);
   MOD_LAUNCH_CHECK();
   const size_t tot = (size_t)BH * p;
   reduce_rhs_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(part, r, p, tiles, BH);
@@ -463,14 +430,16 @@ extern "C" mod_status mod_update_online_mask(mod_plan P, const float* stats_fres
   MOD_REQUIRE(stats_fresh && row_ptr && col_idx && stats_hist && x_prev && x_curr && ws, MOD_ERR_USAGE,
               "mod_update_online_mask: all pointers must be non-NULL");
   cudaStream_t s = as_stream(stream);
-  const int BH = P->L.batch * P->L.heads;
+  const int BH = P->L.batch * P->L.heads, n = P->n;
+  merge_kernel<<<dim3((n + 3) / 4, BH), 128, 0, s>>>(stats_fresh, row_ptr, col_idx, stats_hist, n,
+                                                     P->cfg.masked_renorm);
+  MOD_LAUNCH_CHECK();
   double* X = reinterpret_cast<double*>(static_cast<char*>(ws) + P->ws_x);
-  const MergeArgs merge{stats_fresh, row_ptr, col_idx, P->cfg.masked_renorm};
-  st = fit_from_map(P, stats_hist, X, ws, s, &merge);   // Eq. 5 merge fused into the fit's projection
+  st = fit_from_map(P, stats_hist, X, ws, s);
   if (st != MOD_OK) return st;
   const size_t tot = (size_t)BH * P->p;
   roll_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(x_prev, x_curr, X, tot);
   MOD_LAUNCH_CHECK();
-  mod_note_launches(5);
+  mod_note_launches(6);
   return MOD_OK;
 }
