@@ -380,13 +380,34 @@ __global__ void __launch_bounds__(320, 1)
 #ifndef K4_PREFETCH_Q
 #define K4_PREFETCH_Q 1
 #endif
+// A tile of `rows` token rows x D bf16 of head bh into shared memory as NATOM 128B-swizzled 64-column
+// atoms one `box` apart.  K4_TMA4D (D = 128): ONE 4D TMA box {64 columns, rows, 2 atoms, 1} over the
+// [B*H, N, D] tensor viewed as {64, N, D/64, B*H} (make_map_tile), whose shared-memory image is exactly
+// the two atoms back to back -- half the TMA instructions of the producer thread.
+#ifndef K4_TMA4D
+#define K4_TMA4D 1
+#endif
 template <int NATOM>
+__device__ __forceinline__ void tma_load_tile(unsigned char* dst, int box, const CUtensorMap* m, uint64_t* bar, int row,
+                                              int bh, uint64_t policy) {
+  if constexpr (K4_TMA4D && NATOM == 2) {
+    tma_load_4d(dst, m, bar, 0, row, 0, bh, policy);
+  } else {
+#pragma unroll
+    for (int a = 0; a < NATOM; ++a) tma_load_3d(dst + a * box, m, bar, a * 64, row, bh, policy);
+  }
+}
+template <int NATOM, bool TILE_MAP = false>   // TILE_MAP: tm_q was made by make_map_tile
 __device__ __forceinline__ void prefetch_next_q(const CUtensorMap* tm_q, int item, int n, int block) {
   if constexpr (K4_PREFETCH_Q) {
     const int nx = item + (int)num_sms();
     if (nx < (int)gridDim.x) {
+      if constexpr (TILE_MAP && K4_TMA4D && NATOM == 2) {
+        tma_prefetch_l2_4d(tm_q, 0, (nx % n) * block, 0, nx / n);
+      } else {
 #pragma unroll
-      for (int a = 0; a < NATOM; ++a) tma_prefetch_l2_3d(tm_q, a * 64, (nx % n) * block, nx / n);
+        for (int a = 0; a < NATOM; ++a) tma_prefetch_l2_3d(tm_q, a * 64, (nx % n) * block, nx / n);
+      }
     }
   }
 }
@@ -558,17 +579,13 @@ __global__ void __launch_bounds__(Attn1Cfg<D, BN>::THREADS, 1)
     const int s = j % NS;
     unsigned char* dst = smem + C::OFF_K + s * C::KV_BYTES;
     mbar_arrive_expect_tx(&k_full[s], C::KV_BYTES);
-    const int row = cols[j] * block;
-#pragma unroll
-    for (int a = 0; a < C::NATOM; ++a) tma_load_3d(dst + a * C::KV_BOX, &tm_k, &k_full[s], a * 64, row, bh, pol_kv);
+    tma_load_tile<C::NATOM>(dst, C::KV_BOX, &tm_k, &k_full[s], cols[j] * block, bh, pol_kv);
   };
   auto load_v = [&](int j) {   // one thread
     const int s = j & 1;
     unsigned char* dst = smem + C::OFF_V + s * C::KV_BYTES;
     mbar_arrive_expect_tx(&v_full[s], C::KV_BYTES);
-    const int row = cols[j] * block;
-#pragma unroll
-    for (int a = 0; a < C::NATOM; ++a) tma_load_3d(dst + a * C::KV_BOX, &tm_v, &v_full[s], a * 64, row, bh, pol_kv);
+    tma_load_tile<C::NATOM>(dst, C::KV_BOX, &tm_v, &v_full[s], cols[j] * block, bh, pol_kv);
   };
   // S_j = Q K_j^T into S buffer b = j % NS; whole warp, converged (elect.sync inside each MMA keeps the
   // descriptors in uniform registers)
@@ -614,12 +631,10 @@ __global__ void __launch_bounds__(Attn1Cfg<D, BN>::THREADS, 1)
       tma_prefetch_desc(&tm_k);
       tma_prefetch_desc(&tm_v);
       mbar_arrive_expect_tx(q_full, C::Q_BYTES);
-#pragma unroll
-      for (int a = 0; a < C::NATOM; ++a)
-        tma_load_3d(smem + C::OFF_Q + a * C::Q_BOX, &tm_q, q_full, a * 64, qi * block, bh, pol_q);
+      tma_load_tile<C::NATOM>(smem + C::OFF_Q, C::Q_BOX, &tm_q, q_full, qi * block, bh, pol_q);
       // demand order of the MMA warps: K_0 .. K_{NS-1}, then V_j, K_{j+NS} for j = 0, 1, ...
       for (int j = 0; j < NS && j < L; ++j) load_k(j);
-      prefetch_next_q<C::NATOM>(&tm_q, item, n, block);
+      prefetch_next_q<C::NATOM, true>(&tm_q, item, n, block);
       for (int j = 0; j < L; ++j) {
         if (j >= 2) K4_WAIT(&o_done[(j - 2) % NS], ((j - 2) / NS) & 1);   // PV_{j-2} has consumed V slot j % 2
         load_v(j);
@@ -1449,6 +1464,24 @@ mod_status make_map(CUtensorMap* m, const void* base, int BH, int N, int D, int 
   return MOD_OK;
 }
 
+// The tensor map tma_load_tile expects: 3D {D, N, BH} with {64, rows, 1} boxes, or for D = 128 with K4_TMA4D
+// the 4D view {64, N, 2, BH} (strides D*2, 128, N*D*2 bytes) with {64, rows, 2, 1} boxes.
+mod_status make_map_tile(CUtensorMap* m, const void* base, int BH, int N, int D, int rows) {
+  if (!(K4_TMA4D && D == 128)) return make_map(m, base, BH, N, D, rows);
+  auto enc = get_encode();
+  MOD_REQUIRE(enc, MOD_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled driver entry point unavailable");
+  MOD_REQUIRE(((uintptr_t)base & 127) == 0, MOD_ERR_INPUT, "Q/K/V pointers must be 128-byte aligned");
+  cuuint64_t dims[4] = {64, (cuuint64_t)N, 2, (cuuint64_t)BH};
+  cuuint64_t strides[3] = {(cuuint64_t)D * 2, 128, (cuuint64_t)N * D * 2};
+  cuuint32_t box[4] = {64, (cuuint32_t)rows, 2, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  MOD_REQUIRE(r == CUDA_SUCCESS, MOD_ERR_CUDA, "cuTensorMapEncodeTiled (4D tile view) failed (%d)", (int)r);
+  return MOD_OK;
+}
+
 // One launcher for the single-query-block schedules (DEFAULT, SPLITKV): grid = (b, h, query block).
 template <typename Cfg, typename Kern>
 mod_status launch_rows(mod_plan P, Kern kern, int D, int BN, const void* q, const void* k, const void* v,
@@ -1470,7 +1503,20 @@ mod_status launch_rows(mod_plan P, Kern kern, int D, int BN, const void* q, cons
 template <int D, int BN>
 mod_status launch_default(mod_plan P, const void* q, const void* k, const void* v, const int* row_ptr,
                           const int* col_idx, void* o, float* lse, cudaStream_t s) {
-  return launch_rows<Attn1Cfg<D, BN>>(P, attn_fwd_kernel<D, BN>, D, BN, q, k, v, row_ptr, col_idx, o, lse, s);
+  using Cfg = Attn1Cfg<D, BN>;
+  const int BH = P->L.batch * P->L.heads;
+  CUtensorMap tq, tk, tv;
+  mod_status st;
+  if ((st = make_map_tile(&tq, q, BH, P->N, D, Cfg::BM)) != MOD_OK) return st;
+  if ((st = make_map_tile(&tk, k, BH, P->N, D, BN)) != MOD_OK) return st;
+  if ((st = make_map_tile(&tv, v, BH, P->N, D, BN)) != MOD_OK) return st;
+  auto kern = attn_fwd_kernel<D, BN>;
+  MOD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+  const float scale_log2 = P->scale * 1.4426950408889634f;
+  kern<<<BH * P->n, Cfg::THREADS, Cfg::SMEM, s>>>(tq, tk, tv, row_ptr, col_idx, (__nv_bfloat16*)o, lse, P->N, P->n,
+                                                  P->L.block, scale_log2);
+  MOD_LAUNCH_CHECK();
+  return MOD_OK;
 }
 
 template <int D, int BN>
