@@ -374,6 +374,10 @@ __global__ void __launch_bounds__(320, 1)
 #ifndef K4_LANE0_ISSUE
 #define K4_LANE0_ISSUE 1
 #endif
+// P packed in place over the score registers (exp_pack_inplace) in the default schedule's softmax
+#ifndef K4_INPLACE_P
+#define K4_INPLACE_P 1
+#endif
 // Q of the query block one wave ahead (item + number of SMs: the CTA the block scheduler starts about when
 // this one ends) is prefetched into L2 by the producer, so that CTA's first load -- the only HBM read on its
 // critical path (K / V of the head are L2-resident) -- hits L2.
@@ -511,6 +515,29 @@ __device__ __forceinline__ float exp_pack(const float* s, float scale_log2, floa
     }
     acc2[(c / 2) & 1] = fadd2(acc2[(c / 2) & 1], p);
     pk[c / 2] = pack_bf16(p.x, p.y);
+  }
+  return (acc2[0].x + acc2[0].y) + (acc2[1].x + acc2[1].y);
+}
+
+// exp_pack with P packed IN PLACE: the scores r[0..NC) (fp32 bits) become P in r[0..NC/2) (bf16 pairs).  Pair
+// c is read before word c/2 <= c is written, so the packed row lands in the registers the tcgen05.st of P
+// takes without register moves (the score registers are dead after their pair is exponentiated).
+template <int EMU, int NC>
+__device__ __forceinline__ float exp_pack_inplace(uint32_t* r, float scale_log2, float m) {
+  const float2 sc2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-m, -m);
+  float2 acc2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+  for (int c = 0; c < NC; c += 2) {
+    const float2 x = ffma2(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), sc2, nm2);
+    float2 p;
+    if (((c / 2) & 7) < EMU) {
+      p = ex2_poly2<true>(x);
+    } else {
+      p.x = ex2(x.x);
+      p.y = ex2(x.y);
+    }
+    acc2[(c / 2) & 1] = fadd2(acc2[(c / 2) & 1], p);
+    r[c / 2] = pack_bf16(p.x, p.y);
   }
   return (acc2[0].x + acc2[0].y) + (acc2[1].x + acc2[1].y);
 }
@@ -714,6 +741,10 @@ __global__ void __launch_bounds__(Attn1Cfg<D, BN>::THREADS, 1)
         m_run = fmaxf(mx, __shfl_xor_sync(FULL, mx, 16));   // finite: every listed block holds >= 1 key
       }
       if (tr) K4T(trole, 2, j);
+#if K4_INPLACE_P
+      uint32_t* pk = sr;   // P_j packed over the scores (exp_pack_inplace)
+      float sum = exp_pack_inplace<C::EMU, COLS>(sr, scale_log2, m_run);
+#else
       uint32_t pk[COLS / 2];
       float sum;
       if constexpr (C::EMU1 == C::EMU)   // one copy of the loop body (instruction-cache footprint)
@@ -721,17 +752,32 @@ __global__ void __launch_bounds__(Attn1Cfg<D, BN>::THREADS, 1)
       else
         sum = (quarter == 1 || quarter == C::S_WARP % 4) ? exp_pack<C::EMU1, COLS>(s, scale_log2, m_run, pk)
                            : exp_pack<C::EMU, COLS>(s, scale_log2, m_run, pk);
+#endif
       const bool need = !(sum <= C::OVF);
       if (tr) K4T(trole, 3, j);
       if (__any_sync(FULL, need)) {
         // rare: a row maximum moved up by > 20 (log2): exchange half-row maxima, redo against the new m
         const int need_peer = __shfl_xor_sync(FULL, (int)need, 16);   // every lane shuffles (no short-circuit)
         const bool need_row = need || need_peer != 0;
+#if K4_INPLACE_P
+        // the scores were overwritten by P: reload S_j (unchanged in TMEM until P_j is stored) and re-mask
+        tmem_ld_rows<COLS, BN / 2>(tmem + lane_off + b * BN, sr);
+        tmem_ld_wait();
+        if (kv_valid < COLS) {
+#pragma unroll
+          for (int c = 0; c < COLS; ++c)
+            if (c >= kv_valid) s[c] = -INFINITY;
+        }
+#endif
         float rmax = row_max<COLS>(s) * scale_log2;
         rmax = fmaxf(rmax, __shfl_xor_sync(FULL, rmax, 16));
         const float m_new = need_row ? fmaxf(m_run, rmax) : m_run;
         const float alpha = ex2(m_run - m_new);
+#if K4_INPLACE_P
+        sum = exp_pack_inplace<0, COLS>(sr, scale_log2, m_new);   // every lane: its P was overwritten by the reload
+#else
         if (need_row) sum = exp_pack<0, COLS>(s, scale_log2, m_new, pk);
+#endif
         l_run *= alpha;
         m_run = m_new;
         if (j > 0 && __any_sync(FULL, alpha < 1.f)) {
