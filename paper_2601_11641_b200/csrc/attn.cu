@@ -378,6 +378,9 @@ __global__ void __launch_bounds__(320, 1)
 #ifndef K4_INPLACE_P
 #define K4_INPLACE_P 1
 #endif
+#ifndef K4_EARLY_LOADS
+#define K4_EARLY_LOADS 1
+#endif
 // Q of the query block one wave ahead (item + number of SMs: the CTA the block scheduler starts about when
 // this one ends) is prefetched into L2 by the producer, so that CTA's first load -- the only HBM read on its
 // critical path (K / V of the head are L2-resident) -- hits L2.
@@ -583,27 +586,6 @@ __global__ void __launch_bounds__(Attn1Cfg<D, BN>::THREADS, 1)
   const int L = row_ptr[(size_t)bh * (n + 1) + qi + 1] - beg;
   const int* cols = col_idx + (size_t)bh * n * n + beg;
 
-  if (threadIdx.x == 0) {
-    mbar_init(q_full, 1);
-    for (int s = 0; s < NS; ++s) {
-      mbar_init(&k_full[s], 1);
-      mbar_init(&s_full[s], 1);
-      mbar_init(&p_full[s], C::SOFTMAX_WARPS);   // one elected arrival per softmax warp
-      mbar_init(&o_done[s], 1);
-    }
-    for (int s = 0; s < C::VSTAGES; ++s) mbar_init(&v_full[s], 1);
-    fence_mbar_init();
-  }
-#ifdef MOD_K4_TRACE
-  const long long span_c0 = clock64(), span_t0 = gtimer();
-#endif
-  if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  // ---------------------------------------------------------------- loads and MMA issue (warps 0, 1, 10, 11)
   const uint64_t pol_q = policy_evict_first(), pol_kv = policy_evict_last();
   auto load_k = [&](int j) {   // one thread
     const int s = j % NS;
@@ -617,6 +599,38 @@ __global__ void __launch_bounds__(Attn1Cfg<D, BN>::THREADS, 1)
     mbar_arrive_expect_tx(&v_full[s], C::KV_BYTES);
     tma_load_tile<C::NATOM>(dst, C::KV_BOX, &tm_v, &v_full[s], cols[j] * block, bh, pol_kv);
   };
+  auto load_first = [&]() {   // Q and K_0 .. K_{NS-1}: the producer's first loads (one thread)
+    tma_prefetch_desc(&tm_q);
+    tma_prefetch_desc(&tm_k);
+    tma_prefetch_desc(&tm_v);
+    mbar_arrive_expect_tx(q_full, C::Q_BYTES);
+    tma_load_tile<C::NATOM>(smem + C::OFF_Q, C::Q_BOX, &tm_q, q_full, qi * block, bh, pol_q);
+    for (int j = 0; j < NS && j < L; ++j) load_k(j);
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&s_full[s], 1);
+      mbar_init(&p_full[s], C::SOFTMAX_WARPS);   // one elected arrival per softmax warp
+      mbar_init(&o_done[s], 1);
+    }
+    for (int s = 0; s < C::VSTAGES; ++s) mbar_init(&v_full[s], 1);
+    fence_mbar_init();
+    // K4_EARLY_LOADS: the first loads go out before the TMEM allocation and the CTA barrier (thread 0 is the
+    // producer lane), so their latency overlaps the CTA's set-up
+    if (K4_EARLY_LOADS && L > 0) load_first();
+  }
+#ifdef MOD_K4_TRACE
+  const long long span_c0 = clock64(), span_t0 = gtimer();
+#endif
+  if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  // ---------------------------------------------------------------- loads and MMA issue (warps 0, 1, 10, 11)
   // S_j = Q K_j^T into S buffer b = j % NS; whole warp, converged (elect.sync inside each MMA keeps the
   // descriptors in uniform registers)
   auto issue_s = [&](int j, auto bc) {
@@ -657,13 +671,8 @@ __global__ void __launch_bounds__(Attn1Cfg<D, BN>::THREADS, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0 && L > 0) {
-      tma_prefetch_desc(&tm_q);
-      tma_prefetch_desc(&tm_k);
-      tma_prefetch_desc(&tm_v);
-      mbar_arrive_expect_tx(q_full, C::Q_BYTES);
-      tma_load_tile<C::NATOM>(smem + C::OFF_Q, C::Q_BOX, &tm_q, q_full, qi * block, bh, pol_q);
-      // demand order of the MMA warps: K_0 .. K_{NS-1}, then V_j, K_{j+NS} for j = 0, 1, ...
-      for (int j = 0; j < NS && j < L; ++j) load_k(j);
+      // demand order of the MMA warps: Q, K_0 .. K_{NS-1}, then V_j, K_{j+NS} for j = 0, 1, ...
+      if (!K4_EARLY_LOADS) load_first();
       prefetch_next_q<C::NATOM, true>(&tm_q, item, n, block);
       for (int j = 0; j < L; ++j) {
         if (j >= 2) K4_WAIT(&o_done[(j - 2) % NS], ((j - 2) / NS) & 1);   // PV_{j-2} has consumed V slot j % 2
