@@ -931,6 +931,25 @@ __global__ void __launch_bounds__(WideCfg<D, BN>::THREADS, 1)
   const int L = row_ptr[(size_t)bh * (n + 1) + qi + 1] - beg;
   const int* cols = col_idx + (size_t)bh * n * n + beg;
 
+  const uint64_t pol_q = policy_evict_first(), pol_kv = policy_evict_last();
+  auto load_k = [&](int j) {
+    const int s = j % NS;
+    unsigned char* dst = smem + C::OFF_K + s * C::KV_BYTES;
+    mbar_arrive_expect_tx(&k_full[s], C::KV_BYTES);
+    const int row = cols[j] * block;
+#pragma unroll
+    for (int a = 0; a < C::NATOM; ++a) tma_load_3d(dst + a * C::KV_BOX, &tm_k, &k_full[s], a * 64, row, bh, pol_kv);
+  };
+  auto load_first = [&]() {   // Q and K_0 .. K_{NS-1} (one thread)
+    tma_prefetch_desc(&tm_q);
+    tma_prefetch_desc(&tm_k);
+    tma_prefetch_desc(&tm_v);
+    mbar_arrive_expect_tx(q_full, C::Q_BYTES);
+#pragma unroll
+    for (int a = 0; a < C::NATOM; ++a)
+      tma_load_3d(smem + C::OFF_Q + a * C::Q_BOX, &tm_q, q_full, a * 64, qi * block, bh, pol_q);
+    for (int j = 0; j < NS && j < L; ++j) load_k(j);
+  };
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
     for (int s = 0; s < NS; ++s) {
@@ -942,6 +961,7 @@ __global__ void __launch_bounds__(WideCfg<D, BN>::THREADS, 1)
     }
     for (int s = 0; s < C::VSTAGES; ++s) mbar_init(&v_full[s], 1);
     fence_mbar_init();
+    if (K4_EARLY_LOADS && L > 0) load_first();   // before the TMEM allocation and the CTA barrier
   }
   if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_slot);
   tc_fence_before();
@@ -949,15 +969,6 @@ __global__ void __launch_bounds__(WideCfg<D, BN>::THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  const uint64_t pol_q = policy_evict_first(), pol_kv = policy_evict_last();
-  auto load_k = [&](int j) {
-    const int s = j % NS;
-    unsigned char* dst = smem + C::OFF_K + s * C::KV_BYTES;
-    mbar_arrive_expect_tx(&k_full[s], C::KV_BYTES);
-    const int row = cols[j] * block;
-#pragma unroll
-    for (int a = 0; a < C::NATOM; ++a) tma_load_3d(dst + a * C::KV_BOX, &tm_k, &k_full[s], a * 64, row, bh, pol_kv);
-  };
   auto load_v = [&](int j) {
     const int s = j & 1;
     unsigned char* dst = smem + C::OFF_V + s * C::KV_BYTES;
@@ -1005,14 +1016,7 @@ __global__ void __launch_bounds__(WideCfg<D, BN>::THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0 && L > 0) {
-      tma_prefetch_desc(&tm_q);
-      tma_prefetch_desc(&tm_k);
-      tma_prefetch_desc(&tm_v);
-      mbar_arrive_expect_tx(q_full, C::Q_BYTES);
-#pragma unroll
-      for (int a = 0; a < C::NATOM; ++a)
-        tma_load_3d(smem + C::OFF_Q + a * C::Q_BOX, &tm_q, q_full, a * 64, qi * block, bh, pol_q);
-      for (int j = 0; j < NS && j < L; ++j) load_k(j);
+      if (!K4_EARLY_LOADS) load_first();
       prefetch_next_q<C::NATOM>(&tm_q, item, n, block);
       for (int j = 0; j < L; ++j) {
         if (j >= 2) K4_WAIT(&o_done[(j - 2) % NS], ((j - 2) / NS) & 1);
