@@ -78,10 +78,7 @@ typedef enum {
                                blocks: the WIDE schedule (measured faster there) */
   MOD_ATTN_SPLITKV = 1,     /* two 4-warp softmax groups splitting the index list (round-1 kernel) */
   MOD_ATTN_PAIR = 2,        /* two query blocks per CTA walking their merged index list (f4) */
-  MOD_ATTN_WIDE = 3,        /* 16 softmax warps, split-KV over the two key halves of each block (128-token blocks) */
-  MOD_ATTN_ROWSP = 4        /* the DEFAULT roles run by one CTA over two consecutive query blocks, each row's blocks
-                               starting at a ring position that is a multiple of lcm(NS, 2) (pad positions retired
-                               by barrier-only operations): a CTA's fill and drain paid once per two rows */
+  MOD_ATTN_WIDE = 3         /* 16 softmax warps, split-KV over the two key halves of each block (128-token blocks) */
 } mod_attn_kernel;
 
 typedef struct {

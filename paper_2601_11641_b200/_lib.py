@@ -16,9 +16,8 @@ STATUS_NAMES = {0: "MOD_OK", 1: "MOD_ERR_USAGE", 2: "MOD_ERR_INPUT", 3: "MOD_ERR
                 5: "MOD_ERR_UNSUPPORTED"}
 MOD_SELECT_TOPK, MOD_SELECT_THRESHOLD, MOD_SELECT_TOPMASS = 0, 1, 2
 MOD_STAT_POOLED = 0
-MOD_ATTN_DEFAULT, MOD_ATTN_SPLITKV, MOD_ATTN_PAIR, MOD_ATTN_WIDE, MOD_ATTN_ROWSP = range(5)
-ATTN_KERNELS = {"default": MOD_ATTN_DEFAULT, "splitkv": MOD_ATTN_SPLITKV, "pair": MOD_ATTN_PAIR, "wide": MOD_ATTN_WIDE,
-                "rowsp": MOD_ATTN_ROWSP}
+MOD_ATTN_DEFAULT, MOD_ATTN_SPLITKV, MOD_ATTN_PAIR, MOD_ATTN_WIDE = range(4)
+ATTN_KERNELS = {"default": MOD_ATTN_DEFAULT, "splitkv": MOD_ATTN_SPLITKV, "pair": MOD_ATTN_PAIR, "wide": MOD_ATTN_WIDE}
 
 
 class ModLayout(C.Structure):

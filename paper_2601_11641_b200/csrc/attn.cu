@@ -445,19 +445,13 @@ struct Attn1Cfg {
   static constexpr int OCOLS = D / 2;                 // O columns per thread (rescale, epilogue)
   static constexpr int Q_BOX = BM * 128, KV_BOX = BN * 128, NATOM = D / 64;
   static constexpr int Q_BYTES = Q_BOX * NATOM, KV_BYTES = KV_BOX * NATOM;
-#ifndef K4_SMEM_SHIFT
-#define K4_SMEM_SHIFT 0
-#endif
-  static constexpr int OFF_Q = K4_SMEM_SHIFT;   // (SHIFT: layout experiments)
+  static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + Q_BYTES;
   static constexpr int OFF_V = OFF_K + NS * KV_BYTES;
   static constexpr int OFF_BAR = OFF_V + VSTAGES * KV_BYTES;
   // q_full, k_full[NS], v_full[2], s_full[NS], p_full[NS], o_done[NS] (PV_j commits to o_done[j % NS])
   static constexpr int NUM_BARS = 1 + NS + VSTAGES + NS + NS + NS;
-#ifndef K4_EXTRA_SMEM
-#define K4_EXTRA_SMEM 0
-#endif
-  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + K4_EXTRA_SMEM;   // (EXTRA: carve-out experiments)
+  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr int TMEM_O = NS * BN;
   static constexpr uint32_t TMEM_COLS = (NS * BN + D) <= 256 ? 256 : 512;
   static constexpr int SOFTMAX_WARPS = 8;
@@ -869,386 +863,6 @@ __global__ void __launch_bounds__(Attn1Cfg<D, BN>::THREADS, 1)
     g_k4_span[blockIdx.x][3] = ((long long)smid << 32) | (unsigned)L;
   }
 #endif
-}
-
-// ================================================================================================
-// Padded two-row K4 schedule (MOD_ATTN_ROWSP): the default schedule run by one CTA over two consecutive
-// query blocks r0 = 2p, r1 = 2p + 1 of a head WITHOUT per-block bookkeeping.  The two rows' blocks occupy
-// global ring positions g in [S_0, S_0 + L_0) and [S_1, S_1 + L_1) with S_0 = 0 and S_1 = L_0 rounded up to
-// a multiple of UPV = lcm(NS, 2), so each row's unrolled issue loops start at slot 0 (literal S / V slots,
-// loop-invariant descriptors) exactly like the one-row kernel; the <= UPV - 1 positions between the rows are
-// PAD slots retired by barrier-only operations (producer: plain arrivals on k_full / v_full; S issuer: an
-// empty commit of s_full; softmax: an arrival on p_full; PV issuer: an empty commit of o_done), so every
-// barrier keeps its phase sequence.  Per row: Q slot = row (both loaded up front), O accumulator = row when
-// two fit beside the S buffers (D = 64), else one accumulator handed from row 0's epilogue to row 1's first
-// PV through o_free; o_full[row] is committed after the row's last PV.  The fill and drain of a CTA are
-// paid once per two query blocks.
-template <int D, int BN>
-struct RowsPCfg {
-  using A = Attn1Cfg<D, BN>;
-  static constexpr int BM = 128, NS = A::NS, VSTAGES = 2;
-  static constexpr int UPV = (NS % 2) ? 2 * NS : NS;
-  static constexpr int OB = (NS * BN + 2 * D) <= 512 ? 2 : 1;
-  static constexpr int COLS = A::COLS, OCOLS = A::OCOLS;
-  static constexpr int Q_BOX = A::Q_BOX, KV_BOX = A::KV_BOX, NATOM = A::NATOM;
-  static constexpr int Q_BYTES = A::Q_BYTES, KV_BYTES = A::KV_BYTES;
-  static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = OFF_Q + 2 * Q_BYTES;
-  static constexpr int OFF_V = OFF_K + NS * KV_BYTES;
-  static constexpr int OFF_BAR = OFF_V + VSTAGES * KV_BYTES;
-  // q_full[2], k_full[NS], v_full[2], s_full[NS], p_full[NS], o_done[NS], o_full[2], o_free
-  static constexpr int NUM_BARS = 2 + NS + VSTAGES + NS + NS + NS + 2 + 1;
-  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;
-  static_assert(SMEM <= 232448, "RowsPCfg: shared memory");
-  static constexpr int TMEM_O = NS * BN;
-  static constexpr uint32_t TMEM_COLS = (NS * BN + OB * D) <= 256 ? 256 : 512;
-  static constexpr int SOFTMAX_WARPS = 8, S_WARP = 2 + SOFTMAX_WARPS, THREADS = A::THREADS;
-  static constexpr uint32_t IDESC_S = A::IDESC_S, IDESC_O = A::IDESC_O;
-  static constexpr int EMU = A::EMU;
-  static constexpr float OVF = A::OVF;
-};
-
-template <int D, int BN>
-__global__ void __launch_bounds__(RowsPCfg<D, BN>::THREADS, 1)
-    attn_rowsp_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                      const __grid_constant__ CUtensorMap tm_v, const int* __restrict__ row_ptr,
-                      const int* __restrict__ col_idx, __nv_bfloat16* __restrict__ out, float* __restrict__ lse,
-                      int N, int n, int block, float scale_log2) {
-  using C = RowsPCfg<D, BN>;
-  constexpr int NS = C::NS, OB = C::OB, UPV = C::UPV;
-  extern __shared__ __align__(1024) unsigned char smem[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
-  uint64_t* q_full = bars;
-  uint64_t* k_full = q_full + 2;
-  uint64_t* v_full = k_full + NS;
-  uint64_t* s_full = v_full + C::VSTAGES;
-  uint64_t* p_full = s_full + NS;
-  uint64_t* o_done = p_full + NS;
-  uint64_t* o_full = o_done + NS;
-  uint64_t* o_free = o_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 1);
-
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  if (threadIdx.x == 0 && (smem_u32(smem) & 1023u) != 0) __trap();
-  const int npair = (n + 1) >> 1;
-  const int bh = blockIdx.x / npair, r0 = 2 * (blockIdx.x % npair);
-  const bool has1 = r0 + 1 < n;
-  const int* rp = row_ptr + (size_t)bh * (n + 1);
-  const int beg = rp[r0], mid = rp[r0 + 1], end = has1 ? rp[r0 + 2] : mid;
-  const int L0 = mid - beg, L1 = end - mid;
-  // ring position of row 1's first block (pad positions only when row 1 has blocks)
-  const int S1 = L1 > 0 ? (L0 + UPV - 1) / UPV * UPV : L0;
-  const int G = S1 + L1;                       // ring positions used (row 0, pad, row 1)
-  const int* cols0 = col_idx + (size_t)bh * n * n + beg;
-  const int* cols1 = cols0 + L0;
-
-  const uint64_t pol_q = policy_evict_first(), pol_kv = policy_evict_last();
-  // ring position h -> real K / V load, or a pad arrival (one thread)
-  auto produce_k = [&](int h) {
-    if (h >= G) return;
-    const int s = h % NS;
-    if (h < L0 || h >= S1) {
-      const int col = h < L0 ? cols0[h] : cols1[h - S1];
-      unsigned char* dst = smem + C::OFF_K + s * C::KV_BYTES;
-      mbar_arrive_expect_tx(&k_full[s], C::KV_BYTES);
-      tma_load_tile<C::NATOM>(dst, C::KV_BOX, &tm_k, &k_full[s], col * block, bh, pol_kv);
-    } else {
-      mbar_arrive(&k_full[s]);
-    }
-  };
-  auto produce_v = [&](int h, bool real, int col) {
-    const int s = h & 1;
-    if (real) {
-      unsigned char* dst = smem + C::OFF_V + s * C::KV_BYTES;
-      mbar_arrive_expect_tx(&v_full[s], C::KV_BYTES);
-      tma_load_tile<C::NATOM>(dst, C::KV_BOX, &tm_v, &v_full[s], col * block, bh, pol_kv);
-    } else {
-      mbar_arrive(&v_full[s]);
-    }
-  };
-  if (threadIdx.x == 0) {
-    mbar_init(&q_full[0], 1);
-    mbar_init(&q_full[1], 1);
-    mbar_init(&o_full[0], 1);
-    mbar_init(&o_full[1], 1);
-    mbar_init(o_free, C::SOFTMAX_WARPS);
-    for (int s = 0; s < NS; ++s) {
-      mbar_init(&k_full[s], 1);
-      mbar_init(&s_full[s], 1);
-      mbar_init(&p_full[s], C::SOFTMAX_WARPS);
-      mbar_init(&o_done[s], 1);
-    }
-    for (int s = 0; s < C::VSTAGES; ++s) mbar_init(&v_full[s], 1);
-    fence_mbar_init();
-    if (G > 0) {   // first loads before the TMEM allocation and the CTA barrier
-      tma_prefetch_desc(&tm_q);
-      tma_prefetch_desc(&tm_k);
-      tma_prefetch_desc(&tm_v);
-      if (L0 > 0) {
-        mbar_arrive_expect_tx(&q_full[0], C::Q_BYTES);
-        tma_load_tile<C::NATOM>(smem + C::OFF_Q, C::Q_BOX, &tm_q, &q_full[0], r0 * block, bh, pol_q);
-      }
-      for (int h = 0; h < NS; ++h) produce_k(h);
-      if (L1 > 0) {
-        mbar_arrive_expect_tx(&q_full[1], C::Q_BYTES);
-        tma_load_tile<C::NATOM>(smem + C::OFF_Q + C::Q_BYTES, C::Q_BOX, &tm_q, &q_full[1], (r0 + 1) * block, bh, pol_q);
-      }
-    }
-  }
-  if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer: V_g, K_{g+NS} per position g
-    if (lane == 0 && G > 0) {
-      prefetch_next_q<C::NATOM, true>(&tm_q, blockIdx.x, npair, 2 * block);   // (b, h, pair) one wave ahead
-#pragma unroll 1
-      for (int rr = 0; rr < 2; ++rr) {
-        const int s0 = rr ? S1 : 0, Lr = rr ? L1 : L0;
-        const int* cr = rr ? cols1 : cols0;
-#pragma unroll 1
-        for (int j = 0; j < Lr; ++j) {
-          const int g = s0 + j;
-          if (g >= 2) K4_WAIT(&o_done[(g - 2) % NS], ((g - 2) / NS) & 1);   // PV_{g-2} has consumed V slot g % 2
-          produce_v(g, true, cr[j]);
-          if (g + NS < G) {
-            K4_WAIT(&s_full[g % NS], (g / NS) & 1);   // S_g has consumed K slot g % NS
-            if (j + NS < Lr) {
-              const int s = g % NS;
-              unsigned char* dst = smem + C::OFF_K + s * C::KV_BYTES;
-              mbar_arrive_expect_tx(&k_full[s], C::KV_BYTES);
-              tma_load_tile<C::NATOM>(dst, C::KV_BOX, &tm_k, &k_full[s], cr[j + NS] * block, bh, pol_kv);
-            } else {
-              produce_k(g + NS);
-            }
-          }
-        }
-        if (rr == 0) {
-#pragma unroll 1
-          for (int g = L0; g < S1 && g < G; ++g) {   // pad positions between the rows
-            if (g >= 2) K4_WAIT(&o_done[(g - 2) % NS], ((g - 2) / NS) & 1);
-            produce_v(g, false, 0);
-            if (g + NS < G) {
-              K4_WAIT(&s_full[g % NS], (g / NS) & 1);
-              produce_k(g + NS);
-            }
-          }
-        }
-      }
-    }
-  } else if (warp == 1 || warp == C::S_WARP) {
-    // ------------------------------------------------------------ MMA issuers (lane 0)
-    if (G > 0 && lane == 0) {
-      if (warp == 1) {
-        // PV_g: O[row] (+)= P_g V_g; pad positions: an empty commit of o_done
-#pragma unroll 1
-        for (int rr = 0; rr < 2; ++rr) {
-          const int s0 = rr ? S1 : 0, e0 = rr ? G : L0;
-          if (e0 == s0) continue;
-          if (OB == 1 && rr == 1 && L0 > 0) K4_WAIT(o_free, 0);   // row 0's epilogue has read the accumulator
-          const uint32_t d_o = tmem + C::TMEM_O + (OB == 2 && rr ? D : 0);
-          for (int j0 = s0; j0 < e0; j0 += UPV) {
-            static_for<UPV>([&](auto uc) {
-              constexpr int u = decltype(uc)::value, b = u % NS, vs = u % 2;
-              const int g = j0 + u;
-              if (g < e0) {
-                K4_WAIT(&v_full[vs], (g >> 1) & 1);
-                K4_WAIT(&p_full[b], (g / NS) & 1);
-                tc_fence_after();
-                const uint64_t v_base = smem_desc_sw128(smem_u32(smem + C::OFF_V + vs * C::KV_BYTES), C::KV_BOX, 1024);
-                const uint32_t acc0 = g > s0 ? 1u : 0u;
-                static_for<BN / 16>([&](auto kc) {
-                  constexpr int kk = decltype(kc)::value;
-                  k4_mma_ts<kk * 8, kk * 2048 / 16>(d_o, tmem + b * BN, v_base, C::IDESC_O, kk > 0 ? 1u : acc0);
-                });
-                k4_commit(&o_done[b]);
-              }
-            });
-          }
-          k4_commit(&o_full[rr]);
-          if (rr == 0) {
-#pragma unroll 1
-            for (int g = L0; g < S1 && g < G; ++g) {
-              K4_WAIT(&v_full[g & 1], (g >> 1) & 1);
-              K4_WAIT(&p_full[g % NS], (g / NS) & 1);
-              k4_commit(&o_done[g % NS]);
-            }
-          }
-        }
-      } else {
-        // S_g = Q_row K_g^T into S[g % NS] once PV_{g-NS} has completed; pad positions: an empty commit
-#pragma unroll 1
-        for (int rr = 0; rr < 2; ++rr) {
-          const int s0 = rr ? S1 : 0, e0 = rr ? G : L0;
-          if (e0 > s0) {
-            K4_WAIT(&q_full[rr], 0);
-            tc_fence_after();
-            const uint64_t a_base = smem_desc_sw128(smem_u32(smem + C::OFF_Q + rr * C::Q_BYTES), 16, 1024);
-            for (int j0 = s0; j0 < e0; j0 += NS) {
-              static_for<NS>([&](auto uc) {
-                constexpr int b = decltype(uc)::value;
-                const int g = j0 + b;
-                if (g < e0) {
-                  if (g >= NS) {
-                    K4_WAIT(&o_done[b], ((g - NS) / NS) & 1);
-                    tc_fence_after();
-                  }
-                  K4_WAIT(&k_full[b], (g / NS) & 1);
-                  tc_fence_after();
-                  const uint64_t b_base = smem_desc_sw128(smem_u32(smem + C::OFF_K + b * C::KV_BYTES), 16, 1024);
-                  static_for<D / 16>([&](auto kc) {
-                    constexpr int kk = decltype(kc)::value;
-                    k4_mma_ss<((kk / 4) * C::Q_BOX + (kk % 4) * 32) / 16, ((kk / 4) * C::KV_BOX + (kk % 4) * 32) / 16>(
-                        tmem + b * BN, a_base, b_base, C::IDESC_S, kk > 0 ? 1u : 0u);
-                  });
-                  k4_commit(&s_full[b]);
-                }
-              });
-            }
-          }
-          if (rr == 0) {
-#pragma unroll 1
-            for (int g = L0; g < S1 && g < G; ++g) {
-              if (g >= NS) K4_WAIT(&o_done[g % NS], ((g - NS) / NS) & 1);
-              K4_WAIT(&k_full[g % NS], (g / NS) & 1);
-              k4_commit(&s_full[g % NS]);
-            }
-          }
-        }
-      }
-    }
-  } else if (warp < 2 + C::SOFTMAX_WARPS) {
-    // ------------------------------------------------------------ softmax / epilogue, row 0 (+ pad), row 1
-    constexpr int COLS = C::COLS, OCOLS = C::OCOLS, OCH = OCOLS < 32 ? OCOLS : 32;
-    constexpr unsigned FULL = 0xffffffffu;
-    const int quarter = warp & 3;
-    const int h = (warp - 2) >> 2;
-    const int half = lane >> 4;
-    const int row = quarter * 32 + h * 16 + (lane & 15);
-    const uint32_t lane_off = (uint32_t)(quarter * 32 + h * 16) << 16;
-#pragma unroll 1
-    for (int rr = 0; rr < (has1 ? 2 : 1); ++rr) {
-      const int s0 = rr ? S1 : 0, Lr = rr ? L1 : L0;
-      const int* cr = rr ? cols1 : cols0;
-      const uint32_t t_o = tmem + lane_off + C::TMEM_O + (OB == 2 && rr ? D : 0);
-      const int q_row0 = (r0 + rr) * block;
-      const int q_rows = min(block, N - q_row0);
-      float m_run = -INFINITY, l_run = 0.f;
-      int col_next = Lr > 0 ? cr[0] : 0;
-#pragma unroll 1
-      for (int j = 0; j < Lr; ++j) {
-        const int g = s0 + j;
-        const int b = g % NS;
-        const int col = col_next;
-        if (j + 1 < Lr) col_next = cr[j + 1];
-        K4_SWAIT(&s_full[b], (g / NS) & 1);
-        tc_fence_after();
-        uint32_t sr[COLS];
-        tmem_ld_rows<COLS, BN / 2>(tmem + lane_off + b * BN, sr);
-        tmem_ld_wait();
-        float* s = reinterpret_cast<float*>(sr);
-        const int kv_valid = N - col * block - half * COLS;
-        if (kv_valid < COLS) {
-#pragma unroll
-          for (int c = 0; c < COLS; ++c)
-            if (c >= kv_valid) s[c] = -INFINITY;
-        }
-        if (j == 0) {
-          const float mx = row_max<COLS>(s) * scale_log2;
-          m_run = fmaxf(mx, __shfl_xor_sync(FULL, mx, 16));
-        }
-        uint32_t* pk = sr;
-        float sum = exp_pack_inplace<C::EMU, COLS>(sr, scale_log2, m_run);
-        const bool need = !(sum <= C::OVF);
-        if (__any_sync(FULL, need)) {
-          const int need_peer = __shfl_xor_sync(FULL, (int)need, 16);
-          const bool need_row = need || need_peer != 0;
-          tmem_ld_rows<COLS, BN / 2>(tmem + lane_off + b * BN, sr);
-          tmem_ld_wait();
-          if (kv_valid < COLS) {
-#pragma unroll
-            for (int c = 0; c < COLS; ++c)
-              if (c >= kv_valid) s[c] = -INFINITY;
-          }
-          float rmax = row_max<COLS>(s) * scale_log2;
-          rmax = fmaxf(rmax, __shfl_xor_sync(FULL, rmax, 16));
-          const float m_new = need_row ? fmaxf(m_run, rmax) : m_run;
-          const float alpha = ex2(m_run - m_new);
-          sum = exp_pack_inplace<0, COLS>(sr, scale_log2, m_new);
-          l_run *= alpha;
-          m_run = m_new;
-          if (j > 0 && __any_sync(FULL, alpha < 1.f)) {
-            mbar_wait(&o_done[(g - 1) % NS], ((g - 1) / NS) & 1);
-            tc_fence_after();
-#pragma unroll
-            for (int c = 0; c < OCOLS / OCH; ++c) {
-              uint32_t o[OCH];
-              tmem_ld_rows<OCH, D / 2>(t_o + c * OCH, o);
-              tmem_ld_wait();
-#pragma unroll
-              for (int e = 0; e < OCH; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-              tmem_st_rows<OCH, D / 2>(t_o + c * OCH, o);
-            }
-          }
-        }
-        l_run += sum;
-        tmem_st_rows<COLS / 2, BN / 4>(tmem + lane_off + b * BN, pk);
-        tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[b]);
-      }
-      if (rr == 0) {   // pad positions: S committed empty, nothing to exponentiate
-#pragma unroll 1
-        for (int g = L0; g < S1 && g < G; ++g) {
-          K4_SWAIT(&s_full[g % NS], (g / NS) & 1);
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&p_full[g % NS]);
-        }
-      }
-      // epilogue of this row
-      const float l = l_run + __shfl_xor_sync(FULL, l_run, 16);
-      const bool valid = row < q_rows;
-      const size_t grow = (size_t)bh * N + q_row0 + row;
-      if (Lr > 0) {
-        mbar_wait(&o_full[rr], 0);
-        tc_fence_after();
-        uint32_t o[OCOLS];
-        tmem_ld_rows<OCOLS, D / 2>(t_o, o);
-        tmem_ld_wait();
-        if (OB == 1 && rr == 0) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(o_free);
-        }
-        const float inv = 1.0f / l;
-        if (valid) {
-          int4* dst = reinterpret_cast<int4*>(out + grow * D + half * OCOLS);
-#pragma unroll
-          for (int e = 0; e < OCOLS / 8; ++e)
-            dst[e] = make_int4(pack_bf16(__uint_as_float(o[8 * e]) * inv, __uint_as_float(o[8 * e + 1]) * inv),
-                               pack_bf16(__uint_as_float(o[8 * e + 2]) * inv, __uint_as_float(o[8 * e + 3]) * inv),
-                               pack_bf16(__uint_as_float(o[8 * e + 4]) * inv, __uint_as_float(o[8 * e + 5]) * inv),
-                               pack_bf16(__uint_as_float(o[8 * e + 6]) * inv, __uint_as_float(o[8 * e + 7]) * inv));
-          if (lse && half == 0) lse[grow] = (m_run + __log2f(l)) * 0.69314718055994531f;
-        }
-      } else if (valid) {
-        int4* dst = reinterpret_cast<int4*>(out + grow * D + half * OCOLS);
-#pragma unroll
-        for (int e = 0; e < OCOLS / 8; ++e) dst[e] = make_int4(0, 0, 0, 0);
-        if (lse && half == 0) lse[grow] = -INFINITY;
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc<C::TMEM_COLS>(tmem);
-  }
 }
 
 // ================================================================================================
@@ -1968,25 +1582,6 @@ mod_status launch_default(mod_plan P, const void* q, const void* k, const void* 
 }
 
 template <int D, int BN>
-mod_status launch_rowsp(mod_plan P, const void* q, const void* k, const void* v, const int* row_ptr,
-                        const int* col_idx, void* o, float* lse, cudaStream_t s) {
-  using Cfg = RowsPCfg<D, BN>;
-  const int BH = P->L.batch * P->L.heads;
-  CUtensorMap tq, tk, tv;
-  mod_status st;
-  if ((st = make_map_tile(&tq, q, BH, P->N, D, Cfg::BM)) != MOD_OK) return st;
-  if ((st = make_map_tile(&tk, k, BH, P->N, D, BN)) != MOD_OK) return st;
-  if ((st = make_map_tile(&tv, v, BH, P->N, D, BN)) != MOD_OK) return st;
-  auto kern = attn_rowsp_kernel<D, BN>;
-  MOD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-  const float scale_log2 = P->scale * 1.4426950408889634f;
-  kern<<<BH * ((P->n + 1) / 2), Cfg::THREADS, Cfg::SMEM, s>>>(tq, tk, tv, row_ptr, col_idx, (__nv_bfloat16*)o, lse,
-                                                               P->N, P->n, P->L.block, scale_log2);
-  MOD_LAUNCH_CHECK();
-  return MOD_OK;
-}
-
-template <int D, int BN>
 mod_status launch_wide(mod_plan P, const void* q, const void* k, const void* v, const int* row_ptr,
                        const int* col_idx, void* o, float* lse, cudaStream_t s) {
   return launch_rows<WideCfg<D, BN>>(P, attn_wide_kernel<D, BN>, D, BN, q, k, v, row_ptr, col_idx, o, lse, s);
@@ -2058,9 +1653,6 @@ extern "C" const char* mod_attn_kernel_name(mod_plan P) {
                       : (BN == 128 ? "attn_split_kernel<64,128>" : "attn_split_kernel<64,64>");
     case MOD_ATTN_PAIR: return D == 128 ? "attn_pair_kernel<128,128>" : "attn_pair_kernel<64,128>";
     case MOD_ATTN_WIDE: return D == 128 ? "attn_wide_kernel<128,128>" : "attn_wide_kernel<64,128>";
-    case MOD_ATTN_ROWSP:
-      return D == 128 ? (BN == 128 ? "attn_rowsp_kernel<128,128>" : "attn_rowsp_kernel<128,64>")
-                      : (BN == 128 ? "attn_rowsp_kernel<64,128>" : "attn_rowsp_kernel<64,64>");
     default:
       return D == 128 ? (BN == 128 ? "attn_fwd_kernel<128,128>" : "attn_fwd_kernel<128,64>")
                       : (BN == 128 ? "attn_fwd_kernel<64,128>" : "attn_fwd_kernel<64,64>");
@@ -2087,12 +1679,6 @@ extern "C" mod_status mod_block_sparse_attn_fwd(mod_plan P, const void* q, const
     case MOD_ATTN_WIDE:
       st = D == 128 ? launch_wide<128, 128>(P, q, k, v, row_ptr, col_idx, o, lse, s)
                     : launch_wide<64, 128>(P, q, k, v, row_ptr, col_idx, o, lse, s);
-      break;
-    case MOD_ATTN_ROWSP:
-      if (D == 128 && BN == 128) st = launch_rowsp<128, 128>(P, q, k, v, row_ptr, col_idx, o, lse, s);
-      else if (D == 64 && BN == 128) st = launch_rowsp<64, 128>(P, q, k, v, row_ptr, col_idx, o, lse, s);
-      else if (D == 128 && BN == 64) st = launch_rowsp<128, 64>(P, q, k, v, row_ptr, col_idx, o, lse, s);
-      else st = launch_rowsp<64, 64>(P, q, k, v, row_ptr, col_idx, o, lse, s);
       break;
     case MOD_ATTN_SPLITKV:
       if (D == 128 && BN == 128) st = launch_split<128, 128>(P, q, k, v, row_ptr, col_idx, o, lse, s);

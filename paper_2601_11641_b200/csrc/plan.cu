@@ -337,7 +337,7 @@ extern "C" mod_status mod_plan_create(const mod_layout* layout, const mod_config
   MOD_REQUIRE(cfg->select_mode >= 0 && cfg->select_mode <= 2, MOD_ERR_USAGE, "select_mode=%d invalid", cfg->select_mode);
   MOD_REQUIRE(cfg->stat_mode == MOD_STAT_POOLED, MOD_ERR_UNSUPPORTED, "stat_mode=%d not supported", cfg->stat_mode);
   MOD_REQUIRE(cfg->softmax_scale >= 0.f, MOD_ERR_INPUT, "softmax_scale=%g must be >= 0", cfg->softmax_scale);
-  MOD_REQUIRE(cfg->attn_kernel >= MOD_ATTN_DEFAULT && cfg->attn_kernel <= MOD_ATTN_ROWSP, MOD_ERR_USAGE,
+  MOD_REQUIRE(cfg->attn_kernel >= MOD_ATTN_DEFAULT && cfg->attn_kernel <= MOD_ATTN_WIDE, MOD_ERR_USAGE,
               "attn_kernel=%d invalid", cfg->attn_kernel);
 
   int ndev = 0;

@@ -31,7 +31,7 @@ def M():
     return m
 
 
-KERNELS = ["default", "splitkv", "pair", "wide", "rowsp"]
+KERNELS = ["default", "splitkv", "pair", "wide"]
 
 
 @pytest.fixture(params=KERNELS)
@@ -153,7 +153,7 @@ def test_variant_deterministic(M, kern):
     assert torch.equal(o1, o2) and torch.equal(l1, l2)
 
 
-@pytest.mark.parametrize("kern", ["default", "splitkv", "rowsp"])
+@pytest.mark.parametrize("kern", ["default", "splitkv"])
 @pytest.mark.parametrize("w", [syn.TINY, syn.Workload("b64-d128", 1, 2, 128, 0, 2, 10, 13, 64)], ids=lambda w: w.name)
 def test_block64(M, kern, w):
     """64-token blocks (the tiny config, D = 64; and D = 128): more S buffers, half-width softmax rows."""
