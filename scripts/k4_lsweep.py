@@ -15,6 +15,10 @@ import torch
 import synthetic as syn
 import paper_2601_11641_b200 as M
 
+# EXTRA_KERNELS="name=enum,...": schedules of a variant library (MODDIT_LIB_OVERRIDE) the binding does not name
+for spec in filter(None, os.environ.get("EXTRA_KERNELS", "").split(",")):
+    from paper_2601_11641_b200 import _lib
+    _lib.ATTN_KERNELS.setdefault(spec.split("=")[0], int(spec.split("=")[1]))
 cfg = sys.argv[1] if len(sys.argv) > 1 else "cogvideox-5b"
 kerns = (sys.argv[2] if len(sys.argv) > 2 else "default,wide").split(",")
 Ls = [int(x) for x in (sys.argv[3] if len(sys.argv) > 3 else "2,4,8,17,32,64").split(",")]
