@@ -319,6 +319,9 @@ def run_ours(args):
             e_[3].record(st_)
             uev.append(e_)
 
+    overlap_k1 = not (exact or q8 or args.serial_k1)
+    side = torch.cuda.Stream() if overlap_k1 else None
+
     def step(timed_kernels=False):
         if upipe is not None:
             uev.clear()
@@ -332,6 +335,10 @@ def run_ours(args):
         P.predict_block_mask(x_prev0, x_curr0, M_WARMUP - 1, M_WARMUP, t_step, keep, top_k=K, out=(rp, ci))
         if timed_kernels:
             e[1].record(stream)
+        if overlap_k1:   # K1 reads only Q, K: on a side stream beside K4; K3 joins both below
+            side.wait_stream(stream)
+            with torch.cuda.stream(side):
+                P.collect_block_stats(q, k, out=Wf)
         if q8:   # SURVEY f2 (reading Z30): quantize Q, K, V, then INT8 QK^T / FP8 PV attention
             P.quantize_qkv(q, k, v, out=qbuf)
             P.block_sparse_attn_fwd_q8(qbuf, rp, ci, out=o, lse=lse)
@@ -341,6 +348,8 @@ def run_ours(args):
             e[2].record(stream)
         if exact:   # Eq. 2 on the masked map of this step (lse over the kept blocks, reading Z12)
             P.collect_exact_sparsity(q, k, lse, rp, ci, args.eta, out=Wf)
+        elif overlap_k1:
+            stream.wait_stream(side)
         else:
             P.collect_block_stats(q, k, out=Wf)
         P.update_online_mask(Wf, rp, ci, hist, xs_prev, xs_curr)
@@ -496,7 +505,8 @@ def run_ours(args):
                                f"({w_full.frames}x{w_full.height}x{w_full.width}+{w_full.prefix_tokens}), block {blk}",
                    "heads_per_rank": Hl, "top_k": K, "block_sparsity": round(sp, 4),
                    "target_sparsity": args.sparsity, "nnz_blocks_rank0": nnz_local,
-                   "step": "predict(K2b) + attn(K4) + stats(K1) + update(K3: Eq.5 + fit K2a + roll) at t_p=22",
+                   "step": ("predict(K2b) + attn(K4) + stats(K1) + update(K3: Eq.5 + fit K2a + roll) at t_p=22"
+                            + (" (K1 on a side stream beside K4)" if overlap_k1 else "")),
                    "l2": "inputs larger than L2 (Q,K,V = %.2f GB per rank > 126 MB)" % (3 * q.numel() * 2 / 1e9),
                    "parallelism": (f"ulysses a2a in {chunks_u} overlapped head chunks + head-parallel x{ws}"
                                    if args.ulysses else
@@ -666,6 +676,8 @@ def main():
     ap.add_argument("--config", default="hunyuanvideo-720p", choices=sorted(syn.CONFIGS))
     ap.add_argument("--sparsity", type=float, default=0.878)
     ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--serial-k1", action="store_true",
+                    help="run K1 after K4 on one stream (default: K1 on a side stream beside K4, K3 joins both)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-chunks", type=int, default=0,
                     help="head chunks of the pipelined e2e leg (0: about 80 MB of upload per chunk)")

@@ -82,6 +82,11 @@ class Schedule:
             self.last_mask = (rp, ci)
             return o, l
         rp, ci = P.predict_block_mask(S.x_prev, S.x_curr, S.t_prev, S.t_curr, t, S.keep, **self.sel)
+        W_side = None
+        if self.is_update_step(t) and self.stat == "pooled":
+            # K1 reads only this step's Q, K: it runs on a side stream beside K4 (its HBM-bound pool pass fills
+            # the SMs' spare issue and bandwidth next to the compute-bound attention); K3 joins both
+            W_side = self._pooled_side(q, k)
         if self.precision == "q8":   # sparse steps on the Sage-style quantized path (reading Z30)
             if self._qbuf is None:
                 self._qbuf = P.quant_buffer()
@@ -90,11 +95,27 @@ class Schedule:
         else:
             o, l = P.block_sparse_attn_fwd(q, k, v, rp, ci, out=out, lse=lse)
         if self.is_update_step(t):
-            W = self._stat(q, k, l, rp, ci)
+            if W_side is not None:
+                torch.cuda.current_stream().wait_stream(self._side)
+                W = W_side
+            else:
+                W = self._stat(q, k, l, rp, ci)
             P.update_online_mask(W, rp, ci, S.hist, S.x_prev, S.x_curr)
             S.t_prev, S.t_curr = S.t_curr, t
         self.last_mask = (rp, ci)
         return o, l
+
+    def _pooled_side(self, q, k):
+        """K1 (pooled statistic) enqueued on the driver's side stream after everything already on the current
+        stream (so the previous step's reads of its output are complete); the caller joins before K3."""
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream()
+        main = torch.cuda.current_stream()
+        self._side.wait_stream(main)
+        with torch.cuda.stream(self._side):
+            W = self.P.collect_block_stats(q, k)
+        W.record_stream(main)
+        return W
 
     def _stat(self, q, k, lse, rp, ci):
         """Block statistic U of this step: POOLED (north_star (1)) or EXACT Eq. 2 from the attention's lse
