@@ -33,7 +33,7 @@ class ScheduleState:
 class Schedule:
     def __init__(self, plan: Plan, T: int = 50, m: int = 12, dt: int = 10, top_k: int | None = None,
                  select_mode: int | None = None, select_param: float | None = None, stat: str = "pooled",
-                 eta: float = 1e-4, precision: str = "bf16"):
+                 eta: float = 1e-4, precision: str = "bf16", overlap_k1: bool = True):
         if not (1 <= m < T) or dt < 1 or m < 2:
             raise ValueError(f"bad schedule T={T} m={m} dt={dt}")
         if stat not in ("pooled", "exact"):
@@ -47,6 +47,7 @@ class Schedule:
                              "renormalised by the sparse attention's lse (reading Z12)")
         self.P, self.T, self.m, self.dt = plan, T, m, dt
         self.stat, self.eta, self.precision = stat, eta, precision
+        self.overlap_k1 = overlap_k1   # K1 on a side stream beside K4 at update steps (pooled statistic)
         self._qbuf = None
         self.sel = dict(top_k=top_k, select_mode=select_mode, select_param=select_param)
         self.state = ScheduleState()
@@ -83,7 +84,7 @@ class Schedule:
             return o, l
         rp, ci = P.predict_block_mask(S.x_prev, S.x_curr, S.t_prev, S.t_curr, t, S.keep, **self.sel)
         W_side = None
-        if self.is_update_step(t) and self.stat == "pooled":
+        if self.is_update_step(t) and self.stat == "pooled" and self.overlap_k1:
             # K1 reads only this step's Q, K: it runs on a side stream beside K4 (its HBM-bound pool pass fills
             # the SMs' spare issue and bandwidth next to the compute-bound attention); K3 joins both
             W_side = self._pooled_side(q, k)

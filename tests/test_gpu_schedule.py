@@ -152,3 +152,25 @@ def test_schedule_q8_same_masks_as_bf16():
             assert d.max().item() <= 0.1 and d.mean().item() <= 6e-3
     with pytest.raises(ValueError, match="stat='pooled'"):
         Schedule(P, precision="q8", stat="exact")
+
+
+def test_schedule_k1_side_stream_bitwise_equal_to_serial():
+    """K1 on the side stream beside K4 (the default) changes only the order of independent work: every
+    step's O, lse and mask, and the final history / intensities, equal the serial schedule's bit for bit."""
+    import paper_2601_11641_b200 as M
+    w = syn.Workload("sched-prefix", 1, 3, 128, 40, 3, 20, 19, 128)
+    q, k, v = syn.family_s(w, device="cuda")
+    from paper_2601_11641_b200.schedule import Schedule
+    scheds = [Schedule(M.Plan(w, top_k=6, tau_e=0.0), T=30, m=6, dt=5, overlap_k1=ov) for ov in (True, False)]
+    for t in range(1, 31):
+        qt, kt, vt = syn.family_s(w, step=t, device="cuda") if t > 1 else (q, k, v)
+        res = [s_.step(t, qt, kt, vt) for s_ in scheds]
+        torch.cuda.synchronize()
+        assert torch.equal(res[0][0], res[1][0]) and torch.equal(res[0][1], res[1][1]), t
+        (rpa, cia), (rpb, cib) = scheds[0].last_mask, scheds[1].last_mask
+        assert torch.equal(rpa, rpb), t
+        nnz = rpa[..., -1].cpu()
+        for h in range(w.heads):   # the index lists (the capacity beyond nnz is unspecified)
+            assert torch.equal(cia[0, h, : nnz[0, h]], cib[0, h, : nnz[0, h]]), (t, h)
+    sa, sb = scheds[0].state, scheds[1].state
+    assert torch.equal(sa.hist, sb.hist) and torch.equal(sa.x_prev, sb.x_prev) and torch.equal(sa.x_curr, sb.x_curr)
