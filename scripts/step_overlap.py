@@ -54,12 +54,22 @@ def overlapped():
     P.update_online_mask(Wf, rp, ci, hist, xp, xc)
 
 
+def overlapped_k13():   # K1 and K3 both on the side stream beside K4 (K3 needs only K1 and the mask)
+    P.predict_block_mask(x1, x2, 11, 12, 22, keep, top_k=K, out=(rp, ci))
+    side.wait_stream(main)
+    with torch.cuda.stream(side):
+        P.collect_block_stats(q, k, out=Wf)
+        P.update_online_mask(Wf, rp, ci, hist, xp, xc)
+    P.block_sparse_attn_fwd(q, k, v, rp, ci, out=o, lse=lse)
+    main.wait_stream(side)
+
+
 res = {"config": cfg}
 for _ in range(max(10, 3 * reps)):   # warm up to the power / thermal steady state
     serial()
-times = {"serial": [], "overlapped": []}
+times = {"serial": [], "overlapped": [], "overlapped_k13": []}
 for r in range(4):   # alternating blocks
-    for name, fn in (("serial", serial), ("overlapped", overlapped)):
+    for name, fn in (("serial", serial), ("overlapped", overlapped), ("overlapped_k13", overlapped_k13)):
         fn()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -73,4 +83,5 @@ for name, t in times.items():
     res[name + "_ms"] = t
     res[name + "_mean_ms"] = round(sum(t) / len(t), 4)
 res["gain"] = round(res["serial_mean_ms"] / res["overlapped_mean_ms"] - 1, 4)
+res["gain_k13"] = round(res["serial_mean_ms"] / res["overlapped_k13_mean_ms"] - 1, 4)
 print(json.dumps(res))
